@@ -1,0 +1,183 @@
+/*
+ * svb200.h -- C ABI of the B200 state-vector executor (libsvb200.so).
+ *
+ * Plain pointers and sizes only: no torch / Python types cross this line.
+ * Every state pointer is DEVICE memory holding complex128 amplitudes
+ * (interleaved re, im doubles), laid out exactly like the reference's
+ * `blocks` array: row r = rank r's block of 2^L amplitudes, local bit b
+ * (0 = most significant) has stride 2^(L-1-b)  (svpart/plan.py:3-8,
+ * svpart/kernels/numpy_backend.py:3-4).
+ *
+ * All calls are asynchronous on the given CUDA stream (a cudaStream_t passed
+ * as void*; NULL = legacy default stream) and return SVB_OK or an error
+ * code; svb_last_error() gives the message of the last failure on the
+ * calling thread.  Nothing here allocates device memory: scratch is passed
+ * in by the caller.
+ *
+ * Which reference interface each entry point replaces is cited per function.
+ */
+#ifndef SVB200_H
+#define SVB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVB_OK 0
+#define SVB_EINVAL 1 /* bad width / shape: the reference raises ValueError   */
+#define SVB_ECUDA 2  /* CUDA launch or runtime failure                       */
+#define SVB_ERANGE 3 /* size outside what the kernel supports                */
+
+typedef struct svb_c128 {
+  double re, im;
+} svb_c128;
+
+/* Library identity and last error (thread-local). */
+int svb_abi_version(void);
+const char* svb_last_error(void);
+/* sizeof(svb_op), sizeof(svb_cterm), sizeof(svb_sweep_desc): lets a binding
+ * check its struct mirrors against the compiled library. */
+void svb_abi_sizes(size_t* op, size_t* cterm, size_t* desc);
+
+/* ------------------------------------------------------------------------
+ * 1. Inner kernel plugin: in-place gate application on (ranks, 2^L) blocks.
+ *
+ * Replaces svpart.kernels._core.apply_gate / apply_diagonal
+ * (svpart/kernels/_core.pyx:7-9 and :63-65; dispatcher
+ * svpart/kernels/__init__.py:39-60).  `bits` are local bit positions in
+ * gate-slot order (0 = MSB of the local index); slot i addresses matrix
+ * index bit p-1-i.  `matrix` / `diag` are DEVICE pointers (dim x dim row
+ * major / dim entries).  Returns SVB_EINVAL when dim != 2^p, a bit is out
+ * of range or repeated, or p exceeds max_width (the reference's compiled
+ * core uses max_width = 6, _core.pyx:14-15).
+ * ---------------------------------------------------------------------- */
+int svb_apply_gate(svb_c128* blocks, int64_t ranks, int64_t n,
+                   const svb_c128* matrix, int64_t dim,
+                   const int64_t* bits, int p, int max_width, void* stream);
+
+int svb_apply_diagonal(svb_c128* blocks, int64_t ranks, int64_t n,
+                       const svb_c128* diag, int64_t dim,
+                       const int64_t* bits, int p, int max_width, void* stream);
+
+/* ------------------------------------------------------------------------
+ * 2. Fused leaf sweeps: one ApplyFused task (svpart/executor.py:215-222,
+ *    _apply_fused :123-176) as one or more HBM sweeps.
+ *
+ * A sweep reads every amplitude of the device-resident rows once, applies a
+ * compiled gate program to 2^K-amplitude tiles in shared memory/registers
+ * and writes them back once.  The program (ops, coefficients, per-thread
+ * phase tables, per-tile phase terms) is built on the host by
+ * paper_2509_14098_b200/program.py and lives in device memory at `prog`.
+ * `desc` is a HOST array of `nsweeps` descriptors.  If `norm_out` is not
+ * NULL, the sum of |amp|^2 over the state after each sweep is ADDED to
+ * norm_out[desc[i].norm_slot] (the reference's drift check,
+ * executor.py:220-222).
+ * ---------------------------------------------------------------------- */
+#define SVB_MAX_TILE_BITS 13
+#define SVB_MAX_DEV_BITS 40
+#define SVB_REG_BITS 4
+
+typedef struct svb_op {
+  int32_t kind;   /* SVB_OP_*                                                */
+  int32_t a, b;   /* register slots (0..3)                                   */
+  uint32_t rmask; /* STAGE: tile-local register bits; else register ctl mask */
+  uint64_t pmask; /* thread-uniform predicate (dev_base & pmask) == pval     */
+  uint64_t pval;
+  int32_t coef;   /* offset (complex units) into the coefficient pool         */
+  int32_t tab;    /* offset of a 2^(K-4)-entry per-thread table, or -1        */
+  int32_t ctab;   /* per-tile scalar slot, or -1                              */
+  int32_t tf;     /* first of K-4 per-tile per-thread-bit slots, or -1        */
+  int32_t flags;  /* SVB_F_*                                                  */
+  int32_t pad[3];
+} svb_op;
+
+enum {
+  SVB_OP_STAGE = 1, /* spill registers to smem, reload with new rmask        */
+  SVB_OP_U1 = 2,    /* 2x2 on slot a (+ optional pre-phase)                  */
+  SVB_OP_H = 3,     /* unscaled Hadamard on slot a (+ optional pre-phase)    */
+  SVB_OP_X = 4,     /* bit flip on slot a                                    */
+  SVB_OP_U2 = 5,    /* 4x4 on slots (a, b); a is the matrix MSB              */
+  SVB_OP_PH = 6,    /* phase on amplitudes whose slot-a bit is 1             */
+  SVB_OP_PHALL = 7, /* thread-uniform phase on all register amplitudes       */
+  SVB_OP_SCALE = 8  /* multiply every amplitude by coef[0]                   */
+};
+
+enum {
+  SVB_F_PHASE = 1,     /* U1/H: apply the pre-phase before the gate          */
+  SVB_F_PREG_SHIFT = 4 /* bits 4..7: register slots with a non-unit factor   */
+};
+
+typedef struct svb_cterm { /* ctab[dst] *= c  if (tile_base & mask) == mask */
+  int32_t dst;
+  int32_t pad;
+  uint64_t mask;
+  double re, im;
+} svb_cterm;
+
+typedef struct svb_sweep_desc {
+  int32_t K;                            /* tile bits (4..13)                  */
+  int32_t D;                            /* device index bits (L + log2 rows)  */
+  int32_t tin[SVB_MAX_TILE_BITS];       /* tile bit k -> device bit (load)    */
+  int32_t sw[SVB_MAX_TILE_BITS];        /* smem swizzle image of tile bit k   */
+  int32_t st_dev[SVB_MAX_TILE_BITS];    /* store-order bit i -> device bit    */
+  int32_t st_sw[SVB_MAX_TILE_BITS];     /* store-order bit i -> swizzle image */
+  uint64_t st_flip;                     /* device bits inverted at store      */
+  int32_t op_begin, op_count;           /* ops [op_begin, op_begin+op_count)  */
+  int32_t nctab;                        /* per-tile scalar slots              */
+  int32_t norm_slot;                    /* -1: no norm accumulation           */
+  int64_t ops_off, coef_off, tab_off;   /* byte offsets into prog             */
+  int64_t cterm_off, cofs_off;          /* per-tile terms + CSR offsets       */
+} svb_sweep_desc;
+
+int svb_run_sweeps(svb_c128* state, int64_t rows, int L, const void* prog,
+                   const svb_sweep_desc* desc, int nsweeps, double* norm_out,
+                   int grid_limit, void* stream);
+
+/* ------------------------------------------------------------------------
+ * 3. Qubit remap and layout kernels.
+ *
+ * svb_bitswap: in-place exchange of device-index bits u[i] <-> w[i]
+ *   (index bits counted from the LSB of row*2^L + local).  This is
+ *   Pack -> Exchange -> Unpack (executor.py:224-281) when every rank of the
+ *   swap group lives on this device.
+ * svb_pack_region / svb_unpack_region: copy the sub-block of every row whose
+ *   local bits `lbits` (LSB-indexed) read `sel` into / out of a contiguous
+ *   buffer, elements [off, off+count) of the region in enumeration order.
+ *   Used around the NCCL exchange between devices.
+ * svb_bitperm: out-of-place dst[P(f)] = src[f] where bit k of f moves to
+ *   bit perm[k]; gather/scatter by _storage_to_basis (executor.py:310-343).
+ * ---------------------------------------------------------------------- */
+int svb_bitswap(svb_c128* state, int D, const int32_t* u, const int32_t* w,
+                int m, void* stream);
+
+int svb_pack_region(const svb_c128* state, int64_t rows, int L,
+                    const int32_t* lbits, int m, uint32_t sel, int64_t off,
+                    int64_t count, svb_c128* out, void* stream);
+
+int svb_unpack_region(svb_c128* state, int64_t rows, int L,
+                      const int32_t* lbits, int m, uint32_t sel, int64_t off,
+                      int64_t count, const svb_c128* in, void* stream);
+
+int svb_bitperm(const svb_c128* src, svb_c128* dst, int nbits,
+                const int32_t* perm, void* stream);
+
+/* ------------------------------------------------------------------------
+ * 4. Reductions (executor.py:220 norm; compare :361-372).
+ *
+ * svb_norm2: out[0] += sum |x|^2 (out is a device double).
+ * svb_compare: out[0] = max |a - phi*b| with phi aligned at argmax |a||b|;
+ *   scratch must hold svb_compare_scratch_bytes(n) bytes of device memory.
+ * ---------------------------------------------------------------------- */
+int svb_norm2(const svb_c128* x, int64_t n, double* out, void* stream);
+
+size_t svb_compare_scratch_bytes(int64_t n);
+int svb_compare(const svb_c128* a, const svb_c128* b, int64_t n, double* out,
+                void* scratch, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVB200_H */

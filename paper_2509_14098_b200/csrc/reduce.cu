@@ -1,0 +1,150 @@
+// Reductions: squared norm (drift check, svpart/executor.py:220-222) and the
+// phase-aligned max deviation of compare() (executor.py:361-372).
+#include "common.cuh"
+
+namespace svb {
+namespace {
+
+constexpr int kThreads = 256;
+
+__global__ void k_norm2(const double2* __restrict__ x, int64_t n, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = x[i];
+    s = fma(v.x, v.x, fma(v.y, v.y, s));
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) atomicAdd(out, s);
+}
+
+struct WI {
+  double w;
+  int64_t i;
+};
+
+// larger weight wins; ties go to the smaller index (numpy argmax = first)
+__device__ __forceinline__ WI better(WI a, WI b) {
+  if (b.w > a.w || (b.w == a.w && b.i < a.i)) return b;
+  return a;
+}
+
+__device__ __forceinline__ double cabs_(double2 z) { return hypot(z.x, z.y); }
+
+__global__ void k_argmax_w(const double2* __restrict__ a, const double2* __restrict__ b, int64_t n,
+                           WI* part) {
+  __shared__ WI sh[kThreads];
+  WI best{-1.0, INT64_MAX};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    best = better(best, WI{cabs_(a[i]) * cabs_(b[i]), i});
+  }
+  sh[threadIdx.x] = best;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] = better(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+// reduce partials, derive phi, then max |a - phi b| per block
+__global__ void k_maxdev(const double2* __restrict__ a, const double2* __restrict__ b, int64_t n,
+                         const WI* part, int nparts, double* dpart) {
+  __shared__ WI sh[kThreads];
+  __shared__ double2 phi_s;
+  WI best{-1.0, INT64_MAX};
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) best = better(best, part[i]);
+  sh[threadIdx.x] = best;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] = better(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double2 phi = make_double2(1.0, 0.0);
+    if (sh[0].w > 0.0) {
+      const double2 ak = a[sh[0].i], bk = b[sh[0].i];
+      // z = a_k * conj(b_k); phi = z / |z|
+      const double2 z = make_double2(ak.x * bk.x + ak.y * bk.y, ak.y * bk.x - ak.x * bk.y);
+      const double az = cabs_(z);
+      phi = make_double2(z.x / az, z.y / az);
+    }
+    phi_s = phi;
+  }
+  __syncthreads();
+  const double2 phi = phi_s;
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 bi = b[i], ai = a[i];
+    const double2 pb = make_double2(phi.x * bi.x - phi.y * bi.y, phi.x * bi.y + phi.y * bi.x);
+    m = fmax(m, cabs_(make_double2(ai.x - pb.x, ai.y - pb.y)));
+  }
+  __shared__ double shm[kThreads];
+  shm[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) shm[threadIdx.x] = fmax(shm[threadIdx.x], shm[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) dpart[blockIdx.x] = shm[0];
+}
+
+__global__ void k_max_final(const double* dpart, int nparts, double* out) {
+  __shared__ double shm[kThreads];
+  double m = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) m = fmax(m, dpart[i]);
+  shm[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) shm[threadIdx.x] = fmax(shm[threadIdx.x], shm[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = shm[0];
+}
+
+int nblocks(int64_t n) {
+  int64_t b = (n + kThreads - 1) / kThreads;
+  if (b > kNumSMs * 8) b = kNumSMs * 8;
+  return b > 0 ? (int)b : 1;
+}
+
+}  // namespace
+}  // namespace svb
+
+using namespace svb;
+
+extern "C" int svb_norm2(const svb_c128* x, int64_t n, double* out, void* stream) {
+  if (n < 0) return SVB_EINVAL;
+  if (n == 0) return SVB_OK;
+  k_norm2<<<nblocks(n), kThreads, 0, as_stream(stream)>>>(reinterpret_cast<const double2*>(x), n,
+                                                          out);
+  SVB_CHECK_LAUNCH("svb_norm2");
+  return SVB_OK;
+}
+
+extern "C" size_t svb_compare_scratch_bytes(int64_t n) {
+  const int nb = nblocks(n);
+  return sizeof(WI) * nb + sizeof(double) * nb;
+}
+
+extern "C" int svb_compare(const svb_c128* a, const svb_c128* b, int64_t n, double* out,
+                           void* scratch, void* stream) {
+  if (n <= 0) {
+    set_error("compare: empty vectors");
+    return SVB_EINVAL;
+  }
+  const int nb = nblocks(n);
+  WI* part = static_cast<WI*>(scratch);
+  double* dpart = reinterpret_cast<double*>(part + nb);
+  cudaStream_t st = as_stream(stream);
+  auto A = reinterpret_cast<const double2*>(a);
+  auto B = reinterpret_cast<const double2*>(b);
+  k_argmax_w<<<nb, kThreads, 0, st>>>(A, B, n, part);
+  k_maxdev<<<nb, kThreads, 0, st>>>(A, B, n, part, nb, dpart);
+  k_max_final<<<1, kThreads, 0, st>>>(dpart, nb, out);
+  SVB_CHECK_LAUNCH("svb_compare");
+  return SVB_OK;
+}

@@ -1,0 +1,470 @@
+"""Drop-in replacement for the reference's simulation path.
+
+Mirrors ``svpart/executor.py`` (``run_plan`` :179-307, ``gather`` :320,
+``scatter`` :329, ``compare`` :361, ``sample`` :375, ``oracle_simulate``
+:346): same names, argument meaning, result types and exceptions.  The
+difference is where the state lives and how tasks execute:
+
+* the state is a complex128 CUDA tensor of shape (rows, 2^L); one process per
+  GPU holds 2^g / world consecutive ranks as rows (all ranks on one GPU when
+  not running distributed);
+* every ApplyFused task is compiled once (``program.py``) and runs as one
+  fused sweep kernel launch per tile group (``csrc/sweep.cu``);
+* Pack -> Exchange -> Unpack becomes an in-HBM bit swap for ranks on the
+  same GPU and a chunked NCCL exchange between GPUs (``comm.py``);
+* the norm drift check is accumulated on the device inside the sweep and
+  validated once at the end of the run (same exception, same threshold).
+
+There is no CPU execution path: without the CUDA library every call raises.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native
+from . import program as prog
+from .errors import DimensionMismatch, NonUnitaryDrift, PlanInvalid, TooLarge
+
+DRIFT_TOL = 1e-8  # executor.py:221
+
+
+@dataclass
+class DistState:
+    blocks: torch.Tensor  # (rows on this device, 2^L) complex128, CUDA
+    phase: int
+    d: int
+    g: int
+    layouts: list
+    rank_base: int = 0  # global rank id of row 0
+    world: int = 1
+    group: object = None
+
+
+@dataclass
+class RunStats:
+    task_counts: dict
+    compute_seconds: float
+    exchange_seconds: float
+    amps_moved: int
+    bytes_moved: int
+    exchanges: list
+    compile_seconds: float = 0.0
+    sweeps: int = 0
+    kernel_launches: int = 0
+
+
+@dataclass
+class RunResult:
+    state: DistState
+    histogram: dict | None
+    stats: RunStats
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _require_cuda(device=None) -> torch.device:
+    _native.load()
+    if not torch.cuda.is_available():
+        raise _native.NativeError("CUDA device required: the B200 executor has no CPU path")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def _dist_info(group=None):
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+@dataclass
+class _Compiled:
+    blob: torch.Tensor
+    descs: np.ndarray
+    task_sweeps: dict  # task id -> (first desc, count)
+    n_fused: int
+    compile_seconds: float
+    host_blob: np.ndarray = field(repr=False, default=None)
+
+
+_compile_cache: dict = {}
+
+
+def compile_plan(plan, geo: prog.DeviceGeometry, device) -> _Compiled:
+    """Compile every ApplyFused task of the plan for this device (cached)."""
+    import time
+
+    key = (id(plan), len(plan.tasks), geo.d, geo.g, geo.h, geo.rank_base, str(device))
+    hit = _compile_cache.get(key)
+    if hit is not None and hit[0] is plan:
+        return hit[1]
+    t0 = time.perf_counter()
+    buf = prog.ProgramBuffers()
+    task_sweeps = {}
+    slot = 0
+    for task in plan.tasks:
+        if task.kind != "ApplyFused":
+            continue
+        layout = plan.layout_phases[task.payload["phase"]]
+        first = len(buf.descs)
+        n = prog.compile_leaf(task.payload, layout, geo, slot, buf)
+        task_sweeps[task.id] = (first, n, slot)
+        slot += 1
+    blob, descs, _ = prog.pack(buf)
+    host = np.ascontiguousarray(blob)
+    dev_blob = torch.from_numpy(host).to(device)
+    out = _Compiled(dev_blob, descs, task_sweeps, slot, time.perf_counter() - t0, host)
+    _compile_cache.clear()  # keep one plan resident
+    _compile_cache[key] = (plan, out)
+    return out
+
+
+def _storage_bitperm(layout, d: int, to_basis: bool) -> list:
+    """Bit map of _storage_to_basis (executor.py:310-317), LSB-indexed."""
+    perm = [0] * d
+    for q in range(d):
+        s_bit = d - 1 - layout[q]
+        b_bit = d - 1 - q
+        if to_basis:
+            perm[s_bit] = b_bit
+        else:
+            perm[b_bit] = s_bit
+    return perm
+
+
+def _bitperm(src: torch.Tensor, dst: torch.Tensor, perm: list) -> None:
+    lib = _native.load()
+    arr, p32 = _native.i32_array(perm)
+    _native.check(
+        lib.svb_bitperm(src.data_ptr(), dst.data_ptr(), len(perm), p32, _stream_ptr(src.device)),
+        "svb_bitperm",
+    )
+
+
+class _State:
+    """Device storage with a phantom pad so tiny states still fill 16 amplitudes."""
+
+    def __init__(self, rows: int, L: int, device):
+        self.rows, self.L = rows, L
+        n = rows << L
+        self.buf = torch.zeros(max(n, prog.NREG), dtype=torch.complex128, device=device)
+        self.blocks = self.buf[:n].view(rows, 1 << L)
+
+
+# ---------------------------------------------------------------------------
+# run_plan
+# ---------------------------------------------------------------------------
+
+
+def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=None, *,
+             device=None, group=None, grid_limit: int = 0) -> RunResult:
+    """Interpret the task list on the GPU(s); returns the final state and optional histogram.
+
+    Same contract as ``svpart.executor.run_plan`` (executor.py:179-307).
+    Under ``torch.distributed`` every process holds ``2^g / world`` ranks.
+    """
+    device = _require_cuda(device)
+    lib = _native.load()
+    d, g = plan.d, plan.g
+    L = d - g
+    me, world = _dist_info(group)
+    nranks = 1 << g
+    if world > nranks or nranks % world:
+        raise PlanInvalid(f"{nranks} ranks cannot be split over {world} processes")
+    rows = nranks // world
+    h = rows.bit_length() - 1
+    rank_base = me * rows
+    geo = prog.DeviceGeometry(d=d, g=g, h=h, rank_base=rank_base)
+    # tiny states are padded with zero phantom bits up to one 16-amplitude tile
+    geo_eff = prog.DeviceGeometry(d=d, g=g, h=h, rank_base=rank_base, pad_to=prog.RB)
+    rows_eff = 1 << (geo_eff.D - L)
+    stream = _stream_ptr(device)
+
+    stats = RunStats(task_counts={}, compute_seconds=0.0, exchange_seconds=0.0,
+                     amps_moved=0, bytes_moved=0, exchanges=[])
+
+    # protocol validation happens in task order, like the reference
+    state: _State | None = None
+    packed = None
+    done: set = set()
+    compiled = None
+    norms = None
+    events = []  # (kind, start, end)
+    fused_order = []  # task ids of executed ApplyFused, in order
+
+    def fail(exc):
+        # report an earlier drift first, as the reference would have raised it
+        _check_norms()
+        raise exc
+
+    def _check_norms():
+        if norms is None or not fused_order:
+            return
+        vals = norms.cpu().numpy()
+        if world > 1:
+            t = torch.from_numpy(vals).to(device)
+            import torch.distributed as dist
+
+            dist.all_reduce(t, group=group)
+            vals = t.cpu().numpy()
+        for tid in fused_order:
+            slot = compiled.task_sweeps[tid][2]
+            nv = float(vals[slot])
+            if abs(nv - 1.0) > DRIFT_TOL:
+                raise NonUnitaryDrift(f"norm drifted to {nv!r}")
+
+    for task in plan.tasks:
+        if any(dep not in done for dep in task.deps):
+            fail(PlanInvalid(f"task {task.id} runs before its dependencies"))
+        kind = task.kind
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        if kind == "Alloc":
+            if state is not None:
+                fail(PlanInvalid("double Alloc"))
+            if task.payload["num_ranks"] != nranks or task.payload["block_len"] != 1 << L:
+                fail(PlanInvalid("Alloc payload disagrees with plan shape"))
+            state = _State(rows, L, device)
+            if initial is None:
+                if rank_base == 0:
+                    state.blocks[0, 0] = 1.0
+            else:
+                full = scatter(initial, plan, phase=0, device=device)
+                state.blocks.copy_(full.blocks[rank_base:rank_base + rows])
+                del full
+            compiled = compile_plan(plan, geo_eff, device)
+            stats.compile_seconds = compiled.compile_seconds
+            norms = torch.zeros(max(compiled.n_fused, 1), dtype=torch.float64, device=device)
+        elif kind == "ApplyFused":
+            if state is None:
+                fail(PlanInvalid("compute before Alloc"))
+            first, count, _slot = compiled.task_sweeps[task.id]
+            descs = compiled.descs[first:first + count]
+            rc = lib.svb_run_sweeps(
+                state.buf.data_ptr(), rows_eff, L,
+                compiled.blob.data_ptr(), descs.ctypes.data, count, norms.data_ptr(), grid_limit,
+                stream,
+            )
+            _native.check(rc, "svb_run_sweeps")
+            stats.sweeps += count
+            stats.kernel_launches += count
+            fused_order.append(task.id)
+        elif kind == "Pack":
+            if state is None:
+                fail(PlanInvalid("Pack before Alloc"))
+            if packed is not None:
+                fail(PlanInvalid("Pack while a previous Pack is pending"))
+            packed = {"phase": task.payload["phase"], "swaps": task.payload["swaps"], "sent": False}
+        elif kind == "Exchange":
+            if packed is None or packed["swaps"] != task.payload["swaps"]:
+                fail(PlanInvalid("Exchange without matching Pack"))
+            swaps = task.payload["swaps"]
+            m = len(swaps)
+            launches = _remap(state, swaps, geo, group, stream)
+            stats.kernel_launches += launches
+            moved = nranks * ((1 << m) - 1) * (1 << (L - m))
+            messages = nranks * ((1 << m) - 1)
+            packed["sent"] = True
+            stats.amps_moved += moved
+            stats.bytes_moved += moved * 16
+            stats.exchanges.append({"amps": moved, "bytes": moved * 16, "messages": messages})
+        elif kind == "Unpack":
+            if packed is None or not packed.get("sent"):
+                fail(PlanInvalid("Unpack without a completed Exchange"))
+            packed = None
+        elif kind == "Free":
+            if packed is not None:
+                fail(PlanInvalid("Free with undelivered messages"))
+        else:
+            fail(PlanInvalid(f"unknown task kind {kind!r}"))
+        ev1.record()
+        events.append((kind, ev0, ev1))
+        stats.task_counts[kind] = stats.task_counts.get(kind, 0) + 1
+        done.add(task.id)
+
+    if state is None:
+        raise PlanInvalid("plan never allocated state")
+    torch.cuda.synchronize(device)
+    for kind, e0, e1 in events:
+        sec = e0.elapsed_time(e1) / 1e3
+        if kind in ("Pack", "Exchange", "Unpack"):
+            stats.exchange_seconds += sec
+        elif kind == "ApplyFused":
+            stats.compute_seconds += sec
+    _check_norms()
+
+    dstate = DistState(
+        blocks=state.blocks, phase=len(plan.layout_phases) - 1, d=d, g=g,
+        layouts=[list(p) for p in plan.layout_phases], rank_base=rank_base, world=world,
+        group=group,
+    )
+    histogram = None
+    if shots is not None:
+        histogram = sample(gather(dstate), shots, seed)
+    return RunResult(state=dstate, histogram=histogram, stats=stats)
+
+
+def _remap(state: _State, swaps: list, geo: prog.DeviceGeometry, group, stream) -> int:
+    """Pairwise bit swaps rank_bit <-> local_bit (executor.py:224-281)."""
+    lib = _native.load()
+    L, g, h = geo.L, geo.g, geo.h
+    local_u, local_w, remote = [], [], []
+    for s in swaps:
+        ib = g - 1 - s["rank_bit"]
+        lb = L - 1 - s["local_bit"]
+        if ib < h:
+            local_u.append(L + ib)
+            local_w.append(lb)
+        else:
+            remote.append((ib - h, lb))
+    launches = 0
+    if local_u:
+        D = L + h
+        if (state.rows << L) < prog.NREG:
+            D = max(D, 4)
+        u_arr = np.asarray(local_u, dtype=np.int32)
+        w_arr = np.asarray(local_w, dtype=np.int32)
+        _native.check(
+            lib.svb_bitswap(state.buf.data_ptr(), D, u_arr.ctypes.data_as(_native._pi32),
+                            w_arr.ctypes.data_as(_native._pi32), len(local_u), stream),
+            "svb_bitswap",
+        )
+        launches += 1
+    if remote:
+        from . import comm
+
+        launches += comm.exchange(state, remote, geo, group)
+    return launches
+
+
+# ---------------------------------------------------------------------------
+# layout / verification helpers
+# ---------------------------------------------------------------------------
+
+
+def _all_blocks(state: DistState) -> torch.Tensor:
+    if state.world == 1:
+        return state.blocks
+    import torch.distributed as dist
+
+    parts = [torch.empty_like(state.blocks) for _ in range(state.world)]
+    dist.all_gather(parts, state.blocks.contiguous(), group=state.group)
+    return torch.cat(parts, dim=0)
+
+
+def gather_device(state: DistState) -> torch.Tensor:
+    """Dense qubit-0-most-significant vector on the device (executor.py:320-326)."""
+    blocks = _all_blocks(state)
+    layout = state.layouts[state.phase]
+    d = state.d
+    dense = torch.empty(1 << d, dtype=torch.complex128, device=blocks.device)
+    if d == 0:
+        dense.copy_(blocks.reshape(-1))
+        return dense
+    _bitperm(blocks.contiguous().view(-1), dense, _storage_bitperm(layout, d, to_basis=True))
+    return dense
+
+
+def gather(state: DistState) -> np.ndarray:
+    """Dense host vector, like the reference's gather (executor.py:320-326)."""
+    return gather_device(state).cpu().numpy()
+
+
+def scatter(dense, plan, phase: int = 0, device=None) -> DistState:
+    """Distribute a dense state into rank blocks at the given layout phase (executor.py:329-343)."""
+    device = _require_cuda(device)
+    d, g = plan.d, plan.g
+    shape = tuple(dense.shape)
+    if shape != (1 << d,):
+        raise DimensionMismatch(f"state length {shape} != 2^{d}")
+    if isinstance(dense, torch.Tensor):
+        src = dense.to(device=device, dtype=torch.complex128).contiguous()
+    else:
+        src = torch.from_numpy(np.ascontiguousarray(dense, dtype=np.complex128)).to(device)
+    layout = plan.layout_phases[phase]
+    flat = torch.empty(1 << d, dtype=torch.complex128, device=device)
+    if d == 0:
+        flat.copy_(src)
+    else:
+        _bitperm(src, flat, _storage_bitperm(layout, d, to_basis=False))
+    return DistState(
+        blocks=flat.view(1 << g, 1 << (d - g)), phase=phase, d=d, g=g,
+        layouts=[list(p) for p in plan.layout_phases],
+    )
+
+
+def _as_device_vec(x, device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=torch.complex128).contiguous().view(-1)
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.complex128).reshape(-1)).to(device)
+
+
+def compare(a, b, device=None) -> float:
+    """Max amplitude deviation after aligning global phase at the largest amplitude."""
+    if tuple(a.shape) != tuple(b.shape):
+        raise DimensionMismatch(f"{tuple(a.shape)} vs {tuple(b.shape)}")
+    device = _require_cuda(device if device is not None else (a.device if isinstance(a, torch.Tensor) and a.is_cuda else None))
+    lib = _native.load()
+    A, B = _as_device_vec(a, device), _as_device_vec(b, device)
+    n = A.numel()
+    scratch = torch.empty(int(lib.svb_compare_scratch_bytes(n)), dtype=torch.uint8, device=device)
+    out = torch.zeros(1, dtype=torch.float64, device=device)
+    _native.check(lib.svb_compare(A.data_ptr(), B.data_ptr(), n, out.data_ptr(), scratch.data_ptr(),
+                                  _stream_ptr(device)), "svb_compare")
+    return float(out.item())
+
+
+def fidelity(a, b, device=None) -> float:
+    """|<a|b>|^2 / (<a|a><b|b>) on the device."""
+    device = _require_cuda(device)
+    A, B = _as_device_vec(a, device), _as_device_vec(b, device)
+    ov = torch.vdot(A, B)
+    return float((ov.abs() ** 2 / (torch.vdot(A, A).real * torch.vdot(B, B).real)).item())
+
+
+def sample(dense, shots: int, seed: int | None) -> dict:
+    """Seeded measurement histogram {bitstring: count}, qubit 0 first.
+
+    Bit-identical to the reference (executor.py:375-383): numpy's Generator
+    draws over |amp|^2 of the gathered vector.
+    """
+    if isinstance(dense, torch.Tensor):
+        dense = dense.cpu().numpy()
+    probs = np.abs(dense) ** 2
+    probs = probs / probs.sum()
+    rng = np.random.default_rng(seed)
+    outcomes = rng.choice(len(dense), size=shots, p=probs)
+    values, counts = np.unique(outcomes, return_counts=True)
+    d = len(dense).bit_length() - 1
+    return {format(int(v), f"0{d}b"): int(c) for v, c in zip(values, counts)}
+
+
+def oracle_simulate(circuit, device=None) -> np.ndarray:
+    """Dense reference-order simulation from |0...0>, on the GPU (executor.py:346-358)."""
+    from . import kernels
+
+    d = circuit.num_qubits
+    if d > 14:
+        raise TooLarge(f"oracle capped at 14 qubits, got {d}")
+    device = _require_cuda(device)
+    state = torch.zeros((1, 1 << d), dtype=torch.complex128, device=device)
+    state[0, 0] = 1.0
+    for op in circuit.ops:
+        mat = np.asarray(op.gate.matrix)
+        kernels.apply_gate(state, mat, list(op.qubits))
+    return state.view(-1).cpu().numpy()

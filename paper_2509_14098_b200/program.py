@@ -1,0 +1,744 @@
+"""Host compiler: ApplyFused payload -> device sweep program (ops + tables).
+
+This replaces the reference's per-gate interpretation of an ApplyFused leaf
+(``svpart/executor.py:123-176``) with a one-time translation into the
+program format consumed by the fused sweep kernel (``csrc/sweep.cu``, ABI in
+``include/svb200.h``).  The semantics it must reproduce, gate by gate:
+
+* positions: ``pos = layout[q]``; ``pos < g`` is a rank ("global") slot,
+  otherwise local bit ``pos - g`` with stride ``2^(L-1-(pos-g))``
+  (``plan.py:3-8``); a stale passthrough mark raises ``PlanInvalid``
+  (``executor.py:129-131``);
+* a diagonal gate with global slots applies, per rank, the sub-diagonal with
+  those slots fixed to the rank's bits (``executor.py:142-157``);
+* a non-diagonal gate with global slots must have them all as controls
+  (``executor.py:159-162``) and then acts, on ranks whose global controls are
+  all 1, as the matrix restricted to control=1 (``executor.py:163-176``).
+
+Device coordinates: a device holds ``rows = 2^h`` consecutive ranks as rows
+of one array, so its amplitudes are addressed by a D = L + h bit "device
+index" ``row * 2^L + local`` (bits counted from the LSB).  Rank bits below h
+are row bits (device bits L..D-1); higher rank bits are constant on the
+device and are resolved here, so each device gets its own program.
+
+Within a sweep a 2^K-amplitude tile (K tile bits) is processed per CTA; all
+other device bits are "fixed" bits F.  Dense gates need their targets in the
+tile; diagonal gates are decomposed into phase factors [bits all 1] -> c and
+commuted forward until a dense gate touches one of their bits ("flush"), where
+they are fused into that gate's pre-phase.  SWAP and uncontrolled X are
+virtual (relabel / flip the tile bit and fix it up in the store mapping).
+"""
+
+from __future__ import annotations
+
+import cmath
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import gates as gatelib
+from .errors import PlanInvalid
+
+KMAX = 12  # tile bits per sweep (2 x 64 KB double-buffered in shared memory)
+RB = 4  # register slots per thread
+NREG = 1 << RB
+
+OP_STAGE, OP_U1, OP_H, OP_X, OP_U2, OP_PH, OP_PHALL, OP_SCALE = 1, 2, 3, 4, 5, 6, 7, 8
+F_PHASE = 1
+F_PREG_SHIFT = 4
+
+OP_DTYPE = np.dtype(
+    [
+        ("kind", "<i4"), ("a", "<i4"), ("b", "<i4"), ("rmask", "<u4"),
+        ("pmask", "<u8"), ("pval", "<u8"),
+        ("coef", "<i4"), ("tab", "<i4"), ("ctab", "<i4"), ("tf", "<i4"),
+        ("flags", "<i4"), ("pad", "<i4", (3,)),
+    ]
+)
+CTERM_DTYPE = np.dtype([("dst", "<i4"), ("pad", "<i4"), ("mask", "<u8"), ("re", "<f8"), ("im", "<f8")])
+MAXT = 13
+DESC_DTYPE = np.dtype(
+    [
+        ("K", "<i4"), ("D", "<i4"),
+        ("tin", "<i4", (MAXT,)), ("sw", "<i4", (MAXT,)),
+        ("st_dev", "<i4", (MAXT,)), ("st_sw", "<i4", (MAXT,)),
+        ("st_flip", "<u8"),
+        ("op_begin", "<i4"), ("op_count", "<i4"),
+        ("nctab", "<i4"), ("norm_slot", "<i4"),
+        ("ops_off", "<i8"), ("coef_off", "<i8"), ("tab_off", "<i8"),
+        ("cterm_off", "<i8"), ("cofs_off", "<i8"),
+    ],
+    align=True,
+)
+assert OP_DTYPE.itemsize == 64 and CTERM_DTYPE.itemsize == 32
+
+_H = np.array([[1, 1], [1, -1]], dtype=np.complex128) / math.sqrt(2)
+_X = np.array([[0, 1], [1, 0]], dtype=np.complex128)
+_I2 = np.eye(2, dtype=np.complex128)
+
+
+@dataclass
+class DeviceGeometry:
+    """Which slice of the distributed state one device holds."""
+
+    d: int
+    g: int
+    h: int  # log2(rows on this device)
+    rank_base: int  # global rank id of row 0 (multiple of 2^h)
+    pad_to: int = 0  # tiny states are padded with phantom bits to this many
+
+    @property
+    def L(self) -> int:
+        return self.d - self.g
+
+    @property
+    def D(self) -> int:
+        return max(self.L + self.h, self.pad_to)
+
+
+# ---------------------------------------------------------------------------
+# 1. gate resolution: payload entry -> primitive ops in device-bit terms
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class Dense1:
+    """2x2 on device bit `bit`, applied where all `ctrl` bits equal their value."""
+
+    bit: int
+    m: np.ndarray
+    ctrl: dict  # device bit -> required value (0/1)
+
+
+@dataclass
+class Swap:
+    a: int
+    b: int
+
+
+@dataclass
+class Factor:
+    """Diagonal factor: multiply by c where every bit in `bits` is 1 (0-2 bits)."""
+
+    bits: tuple
+    c: complex
+
+
+def _slot_device_bit(pos: int, geo: DeviceGeometry):
+    """(device_bit, None) for a bit that varies on this device, or (None, value)."""
+    if pos >= geo.g:
+        return geo.L - 1 - (pos - geo.g), None
+    ib = geo.g - 1 - pos  # integer bit of the rank id
+    if ib < geo.h:
+        return geo.L + ib, None
+    return None, (geo.rank_base >> ib) & 1
+
+
+def _decompose_diag(diag: np.ndarray, bits: list) -> list:
+    """Exact multiplicative decomposition of a <=2-bit diagonal into Factors."""
+    p = len(bits)
+    if p == 0:
+        return [Factor((), complex(diag[0]))]
+    if p == 1:
+        d0, d1 = complex(diag[0]), complex(diag[1])
+        out = [Factor((), d0)] if d0 != 1 else []
+        r = d1 / d0 if d0 != 1 else d1
+        if r != 1:
+            out.append(Factor((bits[0],), r))
+        return out
+    if p == 2:
+        # slot 0 = matrix bit 1 (MSB), slot 1 = matrix bit 0
+        d00, d01, d10, d11 = (complex(x) for x in diag)
+        out = []
+        if d00 != 1:
+            out.append(Factor((), d00))
+        c0 = d10 / d00 if d00 != 1 else d10  # slot0 alone
+        c1 = d01 / d00 if d00 != 1 else d01  # slot1 alone
+        if c0 != 1:
+            out.append(Factor((bits[0],), c0))
+        if c1 != 1:
+            out.append(Factor((bits[1],), c1))
+        num = d11 * d00 if d00 != 1 else d11
+        den = d10 * d01
+        c01 = num / den if den != 1 else num
+        if c01 != 1:
+            out.append(Factor((bits[0], bits[1]), c01))
+        return out
+    raise NotImplementedError("diagonal gates wider than 2 device bits are not supported")
+
+
+def _controlled_split(m: np.ndarray, ctl_slots: list, p: int):
+    """If m acts as identity unless all control slots are 1, return the target block."""
+    if not ctl_slots:
+        return None
+    dim = 1 << p
+    ones = 0
+    for s in ctl_slots:
+        ones |= 1 << (p - 1 - s)
+    inside = [i for i in range(dim) if (i & ones) == ones]
+    outside = [i for i in range(dim) if (i & ones) != ones]
+    for i in outside:
+        row = m[i]
+        if row[i] != 1 or np.count_nonzero(row) != 1:
+            return None
+        if np.count_nonzero(m[:, i]) != 1:
+            return None
+    return m[np.ix_(inside, inside)]
+
+
+def resolve_entry(entry: dict, layout, geo: DeviceGeometry) -> list:
+    """Primitive ops for one payload gate, in device-bit terms (executor.py:125-176)."""
+    gate = gatelib.gate(entry["kind"], tuple(entry["params"]))
+    qubits = list(entry["qubits"])
+    positions = [layout[q] for q in qubits]
+    global_slots = [i for i, pos in enumerate(positions) if pos < geo.g]
+    if bool(global_slots) != bool(entry["passthrough"]):
+        raise PlanInvalid(f"stale passthrough mark on {entry}")
+    p = gate.num_qubits
+    if not gate.is_diagonal and global_slots and not set(global_slots) <= gate.controls:
+        raise PlanInvalid(f"{gate.kind} on {qubits} has a non-control global slot")
+
+    slot_bit, slot_const = [], []
+    for pos in positions:
+        b, c = _slot_device_bit(pos, geo)
+        slot_bit.append(b)
+        slot_const.append(c)
+    fixed = [i for i in range(p) if slot_bit[i] is None]
+    free = [i for i in range(p) if slot_bit[i] is not None]
+
+    if gate.is_diagonal:
+        diag = np.asarray(gate.matrix).diagonal().reshape((2,) * p) if p else np.asarray(gate.matrix).diagonal()
+        idx = tuple(slot_const[i] if i in fixed else slice(None) for i in range(p))
+        sub = np.asarray(diag[idx]).reshape(-1)
+        return _decompose_diag(sub, [slot_bit[i] for i in free])
+
+    # non-diagonal: fixed slots are controls (validated above)
+    if any(slot_const[i] == 0 for i in fixed):
+        return []  # a constant-0 control: identity on this device
+    m = np.asarray(gate.matrix).reshape((2,) * (2 * p))
+    idx = [slice(None)] * (2 * p)
+    for i in fixed:
+        idx[i] = 1
+        idx[p + i] = 1
+    k = len(free)
+    sub = np.ascontiguousarray(m[tuple(idx)].reshape(1 << k, 1 << k))
+    free_bits = [slot_bit[i] for i in free]
+    ctl = [j for j, i in enumerate(free) if i in gate.controls]
+    tgt = [j for j in range(k) if j not in ctl]
+    if k == 2 and not ctl and gate.kind == "swap":
+        return [Swap(free_bits[0], free_bits[1])]
+    block = _controlled_split(sub, ctl, k) if ctl else None
+    if block is not None and len(tgt) == 1:
+        return [Dense1(free_bits[tgt[0]], block, {free_bits[j]: 1 for j in ctl})]
+    if k == 1:
+        return [Dense1(free_bits[0], sub, {})]
+    raise NotImplementedError(f"no device decomposition for {gate.kind} on {k} free slots")
+
+
+# ---------------------------------------------------------------------------
+# 2. sweep assembly
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class _Item:
+    """A register-level operation before stage assignment (physical tile bits)."""
+
+    kind: int
+    bits: tuple  # physical tile-local positions needing register slots
+    m: np.ndarray | None = None
+    ctrl: dict = field(default_factory=dict)  # physical device bit -> value
+    factors: list = field(default_factory=list)  # pre-phase factors (physical device bits)
+    h_scaled: bool = False
+
+
+@dataclass
+class SweepProgram:
+    K: int
+    tin: list  # tile-local k -> device bit
+    items: list
+    out_map: dict  # physical device bit -> (reference device bit, flip)
+    norm_slot: int = -1
+    scale: complex = 1.0
+
+
+def _tile_bits_needed(prim) -> set:
+    if isinstance(prim, Dense1):
+        return {prim.bit}
+    if isinstance(prim, Swap):
+        return {prim.a, prim.b}
+    return set()
+
+
+def plan_sweeps(prims: list, geo: DeviceGeometry, kmax: int = KMAX) -> list:
+    """Split a leaf's primitive ops into sweeps whose dense bits fit a tile."""
+    D = geo.D
+    K = min(kmax, D)
+    groups, cur, need = [], [], set()
+    for pr in prims:
+        nb = _tile_bits_needed(pr)
+        if len(need | nb) > K and cur:
+            groups.append((cur, need))
+            cur, need = [], set()
+        cur.append(pr)
+        need |= nb
+    if cur or not groups:
+        groups.append((cur, need))
+    out = []
+    for ops, need in groups:
+        tile = set(need)
+        for b in range(D):  # pad with the lowest device bits (coalescing)
+            if len(tile) >= K:
+                break
+            tile.add(b)
+        out.append((ops, sorted(tile)))
+    return out
+
+
+def build_sweep(prims: list, tile: list, geo: DeviceGeometry) -> SweepProgram:
+    """Phase scheduling + virtual swaps for one sweep (physical-bit items)."""
+    K = len(tile)
+    tile_pos = {b: k for k, b in enumerate(tile)}
+    # reference device bit -> physical device bit / flip (tile bits only)
+    where = {b: b for b in tile}
+    flip = {b: 0 for b in tile}
+    pending: list = []  # Factor in physical device bits
+    items: list = []
+    const = complex(1.0)
+    scale = 1.0
+
+    def phys_factor(f: Factor):
+        """Reference-bit factor -> physical factors; a flipped bit reads b = 1 - p."""
+        nonlocal const
+        c = f.c
+        bits_p = [where.get(b, b) for b in f.bits]
+        fl = [flip.get(b, 0) for b in f.bits]
+        if not bits_p:
+            const *= c
+            return []
+        if len(bits_p) == 1:
+            if fl[0]:  # c^(1-p) = c * (1/c)^p
+                const *= c
+                return [Factor((bits_p[0],), 1 / c)]
+            return [Factor((bits_p[0],), c)]
+        a, b = bits_p
+        fa, fb = fl
+        if not fa and not fb:
+            return [Factor((a, b), c)]
+        if fa and not fb:  # c^((1-pa) pb) = c^pb * (1/c)^(pa pb)
+            return [Factor((b,), c), Factor((a, b), 1 / c)]
+        if fb and not fa:
+            return [Factor((a,), c), Factor((a, b), 1 / c)]
+        # c^((1-pa)(1-pb)) = c * (1/c)^pa * (1/c)^pb * c^(pa pb)
+        const *= c
+        return [Factor((a,), 1 / c), Factor((b,), 1 / c), Factor((a, b), c)]
+
+    def flush(pb: int) -> list:
+        nonlocal pending
+        hit = [f for f in pending if pb in f.bits]
+        pending = [f for f in pending if pb not in f.bits]
+        return hit
+
+    for pr in prims:
+        if isinstance(pr, Factor):
+            for f in phys_factor(pr):
+                if f.bits:
+                    pending.append(f)
+                else:
+                    const *= f.c
+            continue
+        if isinstance(pr, Swap):
+            a, b = pr.a, pr.b
+            where[a], where[b] = where[b], where[a]
+            flip[a], flip[b] = flip[b], flip[a]
+            continue
+        assert isinstance(pr, Dense1)
+        pb = where[pr.bit]
+        m = pr.m
+        if flip[pr.bit]:
+            m = _X @ m @ _X
+        ctrl = {}
+        for cb, val in pr.ctrl.items():
+            ctrl[where.get(cb, cb)] = val ^ flip.get(cb, 0)
+        if not ctrl and np.array_equal(m, _X):
+            flip[pr.bit] ^= 1  # virtual: relabel the bit value
+            continue
+        fl = flush(pb)
+        if np.array_equal(m, _X):
+            # the flush must precede the data movement
+            if fl:
+                items.append(_Item(OP_PH, (tile_pos[pb],), factors=fl))
+            items.append(_Item(OP_X, (tile_pos[pb],), ctrl=ctrl))
+            continue
+        is_h = not ctrl and np.array_equal(m, _H)
+        if ctrl and fl:  # a predicated gate cannot carry the (unconditional) pre-phase
+            items.append(_Item(OP_PH, (tile_pos[pb],), factors=fl))
+            fl = []
+        if is_h:
+            scale *= 1 / math.sqrt(2)
+            items.append(_Item(OP_H, (tile_pos[pb],), factors=fl, h_scaled=True))
+        else:
+            items.append(_Item(OP_U1, (tile_pos[pb],), m=np.array(m), ctrl=ctrl, factors=fl))
+
+    # leftover phases are applied at the end of the sweep
+    items.append(_Item(OP_PHALL, (), factors=pending))
+    out_map = {}
+    for ref, phys in where.items():
+        out_map[phys] = (ref, flip[ref])
+    sp = SweepProgram(K=K, tin=list(tile), items=items, out_map=out_map)
+    sp.scale = const * scale
+    return sp
+
+
+# ---------------------------------------------------------------------------
+# 3. stage assignment and table generation
+# ---------------------------------------------------------------------------
+
+
+def _independent3(vs) -> bool:
+    a, b, c = vs
+    return all(x != 0 for x in (a, b, c, a ^ b, a ^ c, b ^ c, a ^ b ^ c))
+
+
+def _choose_swizzle(K: int, patterns: list, seed: int = 0) -> list:
+    """Per-tile-bit smem images so every access pattern is bank-conflict free.
+
+    A 16-byte access by 8 lanes is conflict free iff the lanes' addresses
+    differ in the low 3 bits of the (16 B-unit) smem index; each pattern lists
+    the 3 tile bits that vary across a quarter warp.
+    """
+    low = [1 << k if k < 3 else 0 for k in range(K)]
+
+    def ok(lows):
+        return all(_independent3([lows[k] for k in pat]) for pat in patterns if len(pat) == 3)
+
+    base = [(1 << k) if k < 3 else (1 << (k % 3)) for k in range(K)]
+    if ok(base):
+        lows = base
+    else:
+        rng = np.random.default_rng(seed)
+        lows = None
+        for _ in range(4000):
+            cand = [(1 << k) if k < 3 else int(rng.integers(0, 8)) for k in range(K)]
+            if ok(cand):
+                lows = cand
+                break
+        if lows is None:
+            lows = base  # correct, only slower
+    del low
+    return [(1 << k) if k < 3 else ((1 << k) | lows[k]) for k in range(K)]
+
+
+def _stages(items: list) -> list:
+    """Group items into stages of <= 4 register bits; returns [(rbits, items)]."""
+    stages = []
+    cur, need = [], set()
+    for it in items:
+        nb = set(it.bits)
+        if len(need | nb) > RB and cur:
+            stages.append([need, cur])
+            cur, need = [], set()
+        cur.append(it)
+        need |= nb
+    if cur:
+        stages.append([need, cur])
+    return stages
+
+
+@dataclass
+class ProgramBuffers:
+    ops: list = field(default_factory=list)  # dicts -> OP_DTYPE
+    coef: list = field(default_factory=list)  # complex
+    tab: list = field(default_factory=list)  # np arrays (complex)
+    tab_len: int = 0
+    cterms: list = field(default_factory=list)  # (dst, mask, c) per sweep
+    cofs: list = field(default_factory=list)  # int per sweep CSR
+    descs: list = field(default_factory=list)
+
+    def add_coef(self, vals) -> int:
+        off = len(self.coef)
+        self.coef.extend(complex(v) for v in vals)
+        return off
+
+    def add_tab(self, arr: np.ndarray) -> int:
+        off = self.tab_len
+        self.tab.append(np.asarray(arr, dtype=np.complex128))
+        self.tab_len += len(arr)
+        return off
+
+
+def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers) -> None:
+    K = sp.K
+    tin = sp.tin
+    dev_to_tile = {b: k for k, b in enumerate(tin)}
+    NT = 1 << (K - RB)
+    tidx = np.arange(NT, dtype=np.int64)
+
+    items = list(sp.items)
+    # fold the accumulated constant / H scale into the final phase item
+    final = items[-1]
+    assert final.kind == OP_PHALL
+    stages = _stages([it for it in items if it.kind != OP_PHALL])
+    if not stages and (final.factors or sp.scale != 1):
+        stages = [[set(), []]]
+    # pad register sets to exactly RB bits, preferring bits used soon after
+    for si, st in enumerate(stages):
+        need = st[0]
+        for later in stages[si + 1:]:
+            for b in sorted(later[0]):
+                if len(need) < RB and b not in need:
+                    need.add(b)
+        for b in range(K):
+            if len(need) >= RB:
+                break
+            need.add(b)
+        st[0] = need
+    if stages:
+        # leftover factors: anchor those touching a last-stage register bit on
+        # that bit (OP_PH), the rest become one thread-uniform OP_PHALL
+        last_r = stages[-1][0]
+        by_anchor: dict = {}
+        rest_f = []
+        for f in final.factors:
+            ks = [dev_to_tile.get(b) for b in f.bits]
+            regs = [k for k in ks if k is not None and k in last_r]
+            if regs:
+                by_anchor.setdefault(min(regs), []).append(f)
+            else:
+                rest_f.append(f)
+        for k in sorted(by_anchor):
+            stages[-1][1].append(_Item(OP_PH, (k,), factors=by_anchor[k]))
+        stages[-1][1].append(_Item(OP_PHALL, (), factors=rest_f))
+
+    # smem swizzle: load (tile bits 0..2), store order, each stage's thread bits
+    store_order = sorted(range(K), key=lambda k: sp.out_map[tin[k]][0])
+    patterns = [[0, 1, 2], store_order[:3]]
+    for rb, _ in stages:
+        comp = [k for k in range(K) if k not in rb]
+        patterns.append(comp[:3])
+    sw = _choose_swizzle(K, [p for p in patterns if len(p) == 3])
+
+    ctab_terms: dict = {}  # slot -> list of (mask, c)
+    nct = [0]
+
+    def new_ctab() -> int:
+        s = nct[0]
+        nct[0] += 1
+        ctab_terms[s] = []
+        return s
+
+    op_begin = len(buf.ops)
+    for rbits, sitems in stages:
+        rlist = sorted(rbits)
+        slot_of = {k: i for i, k in enumerate(rlist)}
+        comp = [k for k in range(K) if k not in rbits]
+        tbit_of = {k: i for i, k in enumerate(comp)}
+        rmask = 0
+        for k in rlist:
+            rmask |= 1 << k
+        buf.ops.append(dict(kind=OP_STAGE, rmask=rmask))
+        for it in sitems:
+            op = dict(kind=it.kind, a=0, b=0, rmask=0, pmask=0, pval=0, coef=0, tab=-1,
+                      ctab=-1, tf=-1, flags=0)
+            if it.bits:
+                op["a"] = slot_of[it.bits[0]]
+            # controls: register bits -> rmask (slot mask); others -> predicate
+            for cb, val in it.ctrl.items():
+                k = dev_to_tile.get(cb)
+                if k is not None and k in slot_of:
+                    op["rmask"] |= 1 << slot_of[k]
+                    op["b"] |= val << slot_of[k]
+                else:
+                    op["pmask"] |= 1 << cb
+                    op["pval"] |= val << cb
+            # phase factors -> (const, per-thread table, per-tile slots, register factors)
+            pre_const = complex(1.0)
+            preg = [complex(1.0)] * RB
+            tab = None
+            tf_terms: dict = {}
+            scal_terms: list = []
+            anchor = it.bits[0] if it.bits else None
+            for f in it.factors:
+                rest = [b for b in f.bits if not (anchor is not None and dev_to_tile.get(b) == anchor)]
+                if anchor is not None and len(rest) == len(f.bits):
+                    raise AssertionError("flushed factor does not touch its anchor bit")
+                if not rest:
+                    pre_const *= f.c
+                    continue
+                if len(rest) == 1:
+                    b = rest[0]
+                    k = dev_to_tile.get(b)
+                    if k is not None and k in slot_of:
+                        if anchor is None:
+                            raise AssertionError("register factor without anchor")
+                        preg[slot_of[k]] *= f.c
+                    elif k is not None:
+                        if tab is None:
+                            tab = np.ones(NT, dtype=np.complex128)
+                        tab[((tidx >> tbit_of[k]) & 1) == 1] *= f.c
+                    else:
+                        scal_terms.append((1 << b, f.c))
+                    continue
+                # two bits, no anchor (final PHALL / PH item)
+                b0, b1 = rest
+                k0, k1 = dev_to_tile.get(b0), dev_to_tile.get(b1)
+                in0 = k0 is not None and k0 in slot_of
+                in1 = k1 is not None and k1 in slot_of
+                if in0 or in1:
+                    raise AssertionError("register factor reached PHALL")
+                if k0 is not None and k1 is not None:
+                    if tab is None:
+                        tab = np.ones(NT, dtype=np.complex128)
+                    sel = (((tidx >> tbit_of[k0]) & 1) == 1) & (((tidx >> tbit_of[k1]) & 1) == 1)
+                    tab[sel] *= f.c
+                elif k0 is None and k1 is None:
+                    scal_terms.append(((1 << b0) | (1 << b1), f.c))
+                else:
+                    kt, bf = (k0, b1) if k0 is not None else (k1, b0)
+                    tf_terms.setdefault(tbit_of[kt], []).append((1 << bf, f.c))
+            if it.kind == OP_PHALL:
+                pre_const *= sp.scale
+            has_phase = bool(it.factors) or it.kind == OP_PHALL
+            if it.kind in (OP_PH, OP_H, OP_U1) and it.factors:
+                if it.kind != OP_PH and (op["pmask"] or (it.kind == OP_H and op["rmask"])):
+                    raise AssertionError("pre-phase on a predicated gate")
+                op["flags"] |= F_PHASE
+            if has_phase:
+                if scal_terms:
+                    s = new_ctab()
+                    ctab_terms[s].extend(scal_terms)
+                    op["ctab"] = s
+                if tf_terms:
+                    first = None
+                    for i in range(K - RB):
+                        s = new_ctab()
+                        if first is None:
+                            first = s
+                        ctab_terms[s].extend(tf_terms.get(i, []))
+                    op["tf"] = first
+                if tab is not None:
+                    op["tab"] = buf.add_tab(tab)
+                nt = 0
+                for i in range(RB):
+                    if preg[i] != 1:
+                        nt |= 1 << i
+                op["flags"] |= nt << F_PREG_SHIFT
+            if it.kind == OP_PHALL:
+                if not has_phase:
+                    continue
+                if op["ctab"] < 0 and op["tab"] < 0 and op["tf"] < 0:
+                    if pre_const == 1:
+                        continue
+                    op["kind"] = OP_SCALE
+                op["coef"] = buf.add_coef([pre_const])
+            elif it.kind == OP_PH:
+                op["coef"] = buf.add_coef([pre_const] + preg)
+            elif it.kind in (OP_H, OP_U1):
+                m = it.m if it.m is not None else np.eye(2)
+                op["coef"] = buf.add_coef([m[0, 0], m[0, 1], m[1, 0], m[1, 1], pre_const] + preg)
+            elif it.kind == OP_X:
+                pass
+            elif it.kind == OP_U2:
+                a, b = slot_of[it.bits[0]], slot_of[it.bits[1]]
+                mm = np.asarray(it.m)
+                if a > b:  # kernel wants a < b with a as the matrix MSB
+                    perm = [0, 2, 1, 3]
+                    mm = mm[np.ix_(perm, perm)]
+                    a, b = b, a
+                op["a"], op["b"] = a, b
+                op["coef"] = buf.add_coef(mm.reshape(-1))
+            buf.ops.append(op)
+    op_count = len(buf.ops) - op_begin
+
+    # per-tile term CSR for this sweep
+    cofs_base = len(buf.cofs)
+    terms_base = len(buf.cterms)
+    offs = [terms_base]
+    for s in range(nct[0]):
+        for mask, c in ctab_terms[s]:
+            buf.cterms.append((s, mask, c))
+        offs.append(len(buf.cterms))
+    buf.cofs.extend(offs)
+
+    tout = [sp.out_map[tin[k]][0] for k in range(K)]
+    st_flip = 0
+    for k in range(K):
+        if sp.out_map[tin[k]][1]:
+            st_flip |= 1 << tout[k]
+    desc = dict(
+        K=K, D=geo.D, tin=list(tin), sw=sw,
+        st_dev=[tout[k] for k in store_order], st_sw=[sw[k] for k in store_order],
+        st_flip=st_flip, op_begin=op_begin, op_count=op_count, nctab=nct[0],
+        norm_slot=sp.norm_slot, cofs_index=cofs_base,
+    )
+    buf.descs.append(desc)
+
+
+def compile_leaf(payload: dict, layout, geo: DeviceGeometry, norm_slot: int,
+                 buf: ProgramBuffers, kmax: int = KMAX) -> int:
+    """Append the sweeps of one ApplyFused task; returns the number of sweeps."""
+    prims = []
+    for entry in payload["gates"]:
+        prims.extend(resolve_entry(entry, layout, geo))
+    groups = plan_sweeps(prims, geo, kmax)
+    for i, (ops, tile) in enumerate(groups):
+        sp = build_sweep(ops, tile, geo)
+        sp.norm_slot = norm_slot if i == len(groups) - 1 else -1
+        emit_sweep(sp, geo, buf)
+    return len(groups)
+
+
+def pack(buf: ProgramBuffers):
+    """Serialize to (device blob bytes, descriptor array)."""
+    ops = np.zeros(max(len(buf.ops), 1), dtype=OP_DTYPE)
+    for i, o in enumerate(buf.ops):
+        for k, v in o.items():
+            ops[i][k] = v
+    coef = np.array(buf.coef if buf.coef else [0j], dtype=np.complex128)
+    tab = np.concatenate(buf.tab) if buf.tab else np.zeros(1, dtype=np.complex128)
+    ct = np.zeros(max(len(buf.cterms), 1), dtype=CTERM_DTYPE)
+    for i, (dst, mask, c) in enumerate(buf.cterms):
+        ct[i]["dst"] = dst
+        ct[i]["mask"] = mask
+        ct[i]["re"] = c.real
+        ct[i]["im"] = c.imag
+    cofs = np.array(buf.cofs if buf.cofs else [0], dtype=np.int32)
+
+    parts = []
+    off = 0
+
+    def put(arr) -> int:
+        nonlocal off
+        b = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
+        start = off
+        parts.append(b)
+        off += b.size
+        pad = (-off) % 64
+        if pad:
+            parts.append(np.zeros(pad, dtype=np.uint8))
+            off += pad
+        return start
+
+    ops_off = put(ops)
+    coef_off = put(coef)
+    tab_off = put(tab)
+    ct_off = put(ct)
+    cofs_off = put(cofs)
+    blob = np.concatenate(parts) if parts else np.zeros(64, dtype=np.uint8)
+
+    descs = np.zeros(len(buf.descs), dtype=DESC_DTYPE)
+    for i, d in enumerate(buf.descs):
+        e = descs[i]
+        e["K"], e["D"] = d["K"], d["D"]
+        for name in ("tin", "sw", "st_dev", "st_sw"):
+            arr = np.zeros(MAXT, dtype=np.int32)
+            arr[: len(d[name])] = d[name]
+            e[name] = arr
+        e["st_flip"] = d["st_flip"]
+        e["op_begin"], e["op_count"] = d["op_begin"], d["op_count"]
+        e["nctab"], e["norm_slot"] = d["nctab"], d["norm_slot"]
+        e["ops_off"], e["coef_off"], e["tab_off"] = ops_off, coef_off, tab_off
+        e["cterm_off"] = ct_off
+        e["cofs_off"] = cofs_off + 4 * d["cofs_index"]
+    return blob, descs, dict(ops=ops, coef=coef, tab=tab, cterms=ct, cofs=cofs, cofs_base=cofs_off)

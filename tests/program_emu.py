@@ -1,0 +1,180 @@
+"""Numpy emulator of the fused sweep kernel (csrc/sweep.cu) -- tests only.
+
+Executes a compiled program (paper_2509_14098_b200.program.pack output)
+exactly as the kernel does -- same tile origins, shared-memory swizzle, stage
+mappings, register slots, predicates and phase tables -- but vectorised over
+threads with numpy.  Comparing it with the oracle validates the host
+compiler on machines without a GPU; the GPU parity tests then validate the
+kernel against the same oracle.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2509_14098_b200 import program as prog
+
+RB, NR = prog.RB, prog.NREG
+
+
+def _dep(vals: np.ndarray, bits) -> np.ndarray:
+    out = np.zeros_like(vals, dtype=np.int64)
+    for i, b in enumerate(bits):
+        out |= ((vals >> i) & 1) << b
+    return out
+
+
+def _xor_img(vals: np.ndarray, imgs) -> np.ndarray:
+    out = np.zeros_like(vals, dtype=np.int64)
+    for i, s in enumerate(imgs):
+        out ^= np.where((vals >> i) & 1, s, 0)
+    return out
+
+
+def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None) -> None:
+    """In-place on the flat device state (length 2^D)."""
+    ops_all, coef, tab, cterms, cofs_all = (parts[k] for k in ("ops", "coef", "tab", "cterms", "cofs"))
+    cofs_base = 0
+    for d in descs:
+        K, D = int(d["K"]), int(d["D"])
+        NT = 1 << (K - RB)
+        tin = [int(x) for x in d["tin"][:K]]
+        sw = [int(x) for x in d["sw"][:K]]
+        st_dev = [int(x) for x in d["st_dev"][:K]]
+        st_sw = [int(x) for x in d["st_sw"][:K]]
+        st_flip = int(d["st_flip"])
+        nct = int(d["nctab"])
+        ops = ops_all[int(d["op_begin"]): int(d["op_begin"]) + int(d["op_count"])]
+        ci = (int(d["cofs_off"]) - int(parts["cofs_base"])) // 4
+        cofs = cofs_all[ci: ci + nct + 1]
+        fbits = [b for b in range(D) if b not in tin]
+        c_all = np.arange(1 << K, dtype=np.int64)
+        ld_dev = _dep(c_all, tin)
+        ld_s = _xor_img(c_all, sw)
+        st_d = _dep(c_all, st_dev) ^ st_flip
+        st_s = _xor_img(c_all, st_sw)
+        tix = np.arange(NT, dtype=np.int64)
+        nrm = 0.0
+        for tile_id in range(1 << (D - K)):
+            base = 0
+            for i, b in enumerate(fbits):
+                if (tile_id >> i) & 1:
+                    base |= 1 << b
+            ctab = np.ones(max(nct, 1), dtype=np.complex128)
+            for i in range(nct):
+                for q in range(int(cofs[i]), int(cofs[i + 1])):
+                    ct = cterms[q]
+                    if (base & int(ct["mask"])) == int(ct["mask"]):
+                        ctab[i] *= complex(ct["re"], ct["im"])
+            tile = np.empty(1 << K, dtype=np.complex128)
+            tile[ld_s] = state[base | ld_dev]
+            x = None
+            J = None
+            dev_base = None
+            for op in ops:
+                kind = int(op["kind"])
+                if kind == prog.OP_STAGE:
+                    if x is not None:
+                        tile[J] = x
+                    rm = int(op["rmask"])
+                    regs = [k for k in range(K) if (rm >> k) & 1]
+                    comp = [k for k in range(K) if not (rm >> k) & 1]
+                    jt = _dep(tix, comp)
+                    jv = _dep(np.arange(NR, dtype=np.int64), regs)
+                    jj = jt[:, None] | jv[None, :]
+                    J = _img(jj, sw)
+                    x = tile[J].copy()
+                    dev_base = base | _devmap(jt, tin)
+                    continue
+                pred = (dev_base & int(op["pmask"])) == int(op["pval"])
+                if not pred.any():
+                    continue
+                a = int(op["a"])
+                cf = int(op["coef"])
+                cm, cv = int(op["rmask"]), int(op["b"])
+                xs = x.copy()
+                if kind in (prog.OP_H, prog.OP_U1, prog.OP_PH):
+                    has_phase = kind == prog.OP_PH or (int(op["flags"]) & prog.F_PHASE)
+                    if has_phase:
+                        ph = cf if kind == prog.OP_PH else cf + 4
+                        p = np.full(NT, coef[ph], dtype=np.complex128)
+                        if int(op["ctab"]) >= 0:
+                            p = p * ctab[int(op["ctab"])]
+                        if int(op["tab"]) >= 0:
+                            p = p * tab[int(op["tab"]) + tix]
+                        if int(op["tf"]) >= 0:
+                            for i in range(K - RB):
+                                p = np.where((tix >> i) & 1, p * ctab[int(op["tf"]) + i], p)
+                        nt = (int(op["flags"]) >> prog.F_PREG_SHIFT) & 0xF
+                        for v in range(NR):
+                            if not (v >> a) & 1:
+                                continue
+                            q = p.copy()
+                            for s in range(RB):
+                                if s != a and (v >> s) & 1 and (nt >> s) & 1:
+                                    q = q * coef[ph + 1 + s]
+                            xs[:, v] = xs[:, v] * q
+                    if kind == prog.OP_H:
+                        for v in range(NR):
+                            if (v >> a) & 1 or (v & cm) != cv:
+                                continue
+                            x0, x1 = xs[:, v].copy(), xs[:, v | (1 << a)].copy()
+                            xs[:, v], xs[:, v | (1 << a)] = x0 + x1, x0 - x1
+                    elif kind == prog.OP_U1:
+                        m00, m01, m10, m11 = coef[cf:cf + 4]
+                        for v in range(NR):
+                            if (v >> a) & 1 or (v & cm) != cv:
+                                continue
+                            x0, x1 = xs[:, v].copy(), xs[:, v | (1 << a)].copy()
+                            xs[:, v], xs[:, v | (1 << a)] = m00 * x0 + m01 * x1, m10 * x0 + m11 * x1
+                elif kind == prog.OP_X:
+                    for v in range(NR):
+                        if (v >> a) & 1 or (v & cm) != cv:
+                            continue
+                        x0, x1 = xs[:, v].copy(), xs[:, v | (1 << a)].copy()
+                        xs[:, v], xs[:, v | (1 << a)] = x1, x0
+                elif kind == prog.OP_U2:
+                    b = int(op["b"])
+                    M = coef[cf:cf + 16].reshape(4, 4)
+                    for v in range(NR):
+                        if (v >> a) & 1 or (v >> b) & 1:
+                            continue
+                        idx = [v, v | (1 << b), v | (1 << a), v | (1 << a) | (1 << b)]
+                        y = M @ xs[:, idx].T
+                        xs[:, idx] = y.T
+                elif kind == prog.OP_PHALL:
+                    p = np.full(NT, coef[cf], dtype=np.complex128)
+                    if int(op["ctab"]) >= 0:
+                        p = p * ctab[int(op["ctab"])]
+                    if int(op["tab"]) >= 0:
+                        p = p * tab[int(op["tab"]) + tix]
+                    if int(op["tf"]) >= 0:
+                        for i in range(K - RB):
+                            p = np.where((tix >> i) & 1, p * ctab[int(op["tf"]) + i], p)
+                    xs = xs * p[:, None]
+                elif kind == prog.OP_SCALE:
+                    xs = xs * coef[cf]
+                x = np.where(pred[:, None], xs, x)
+            if x is not None:
+                tile[J] = x
+            vals = tile[st_s]
+            nrm += float(np.sum(np.abs(vals) ** 2))
+            state[base | st_d] = vals
+        slot = int(d["norm_slot"])
+        if norms is not None and slot >= 0:
+            norms[slot] += nrm
+        cofs_base += nct + 1
+
+
+def _img(jj: np.ndarray, sw) -> np.ndarray:
+    out = np.zeros_like(jj)
+    for k, s in enumerate(sw):
+        out ^= np.where((jj >> k) & 1, s, 0)
+    return out
+
+
+def _devmap(jt: np.ndarray, tin) -> np.ndarray:
+    out = np.zeros_like(jt)
+    for k, b in enumerate(tin):
+        out |= ((jt >> k) & 1) << b
+    return out
