@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Benchmark: circuit time and HBM GB/s of the B200 executor vs the host-CPU reference.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload qft|qv|NAME]
+
+One "step" = one full ``run_plan`` of the workload's plan (Alloc from |0..0>,
+every ApplyFused sweep, every remap, norm check).  Plans are the reference
+partitioner's output, generated once by tests/golden/make_golden.py and
+read from plans/ (the partitioner runs unchanged on the host; its time is
+reported separately in plans/plans.json).
+
+Workloads (BASELINE.json configs): at N=1 the 34-qubit configs do not fit one
+B200 (256 GiB of complex128), so the single-GPU line is cfg2, QFT-30 with
+hierarchy [30, 12].  For N > 1 the default is weak scaling: QFT-(30+log2 N)
+with [30, 12], 2^30 amplitudes per GPU and one NCCL remap.  ``--workload qv``
+runs QV-30 (N=1) / QV-34 [34-log2 N, 12] (N = 2, 4, 8: strong scaling).
+
+value   = algorithmic HBM bytes of all partition sweeps (32 B x 2^L per
+          ApplyFused per rank) / device time of the step,
+          summed over ranks; ms_per_step is the circuit time.
+e2e     = the same bytes / time of run_plan(plan, initial=<pinned host
+          state>) plus the device->host copy of the final blocks.
+roofline= the fused sweep kernel (k_sweep): its algorithmic bytes / its
+          CUDA-event time inside the timed steps, against the measured HBM
+          copy bandwidth in MEASURED_PEAKS.json.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "circuit time & HBM GB/s, 34q QFT/QV at 1/2/4/8 B200 vs host-CPU reference"
+UNIT = "GB/s"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def workload_name(kind: str, n: int) -> tuple[str, str]:
+    lg = n.bit_length() - 1
+    if kind == "qft":
+        return f"qft{30 + lg}_h30-12", "weak"
+    if kind == "qv":
+        return ("qv30_h30-12", "strong") if n == 1 else (f"qv34_h{34 - lg}-12", "strong")
+    return kind, "weak"
+
+
+def load_plan(name: str):
+    from paper_2509_14098_b200 import plan as planmod
+
+    return planmod.load(str(ROOT / "plans" / f"{name}.json.gz"))
+
+
+def plan_bytes(plan) -> int:
+    """Algorithmic HBM bytes of all ApplyFused sweeps, whole job."""
+    fused = sum(1 for t in plan.tasks if t.kind == "ApplyFused")
+    return fused * 32 * (1 << plan.d)
+
+
+def peak_hbm() -> tuple[float, str]:
+    try:
+        return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.out = ROOT / "gpurun_out" / f"clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.out.parent.mkdir(exist_ok=True)
+            self.fh = open(self.out, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not self.out.exists():
+            return None
+        rows = []
+        for line in self.out.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm
+# ---------------------------------------------------------------------------
+
+CPU_SAMPLE_PLAN = "qft22_h22-12"  # same family and [d, 12] hierarchy, bounded CPU time
+
+
+def cpu_reference_step(plan, backend: str) -> float:
+    from oracle import oracle as orc
+
+    t0 = time.perf_counter()
+    orc.run_plan(plan, backend=backend, check_norm=True)
+    return time.perf_counter() - t0
+
+
+def cpu_backend() -> tuple[str, str]:
+    ref = ROOT / "oracle" / "_ref"
+    if any(ref.glob("_core*.so")):
+        return "ref", "reference"
+    return "c", "port"
+
+
+def cpu_baseline_line(steps: int = 1, sample: str = CPU_SAMPLE_PLAN) -> dict:
+    plan = load_plan(sample)
+    backend, kind = cpu_backend()
+    times = [cpu_reference_step(plan, backend) for _ in range(max(1, steps))]
+    t = min(times)
+    return {"value": plan_bytes(plan) / t / 1e9, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{sample}: full plan of the same family/hierarchy, reference run_plan "
+                      f"semantics with {'the reference _core.pyx kernels' if kind == 'reference' else 'the C port'}"
+                      f", {plan.d} qubits, best of {len(times)} ({t:.2f} s), host cores {os.cpu_count()}",
+            "seconds": t}
+
+
+def run_reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # only rank 0 runs the CPU baseline under torchrun
+    plan = load_plan(CPU_SAMPLE_PLAN)
+    backend, kind = cpu_backend()
+    for _ in range(args.warmup):
+        cpu_reference_step(plan, backend)
+    times = [cpu_reference_step(plan, backend) for _ in range(args.steps)]
+    total = sum(times)
+    val = plan_bytes(plan) * len(times) / total / 1e9
+    line = {
+        "metric": METRIC, "value": val, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": CPU_SAMPLE_PLAN, "qubits": plan.d, "hierarchy": [plan.d, 12],
+                   "note": "CPU sample of the QFT/[d,12] workload family; reference is single-threaded"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": kind,
+                         "sample": f"{CPU_SAMPLE_PLAN} full plan per step, host cores {os.cpu_count()}"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="qft")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = world
+    name, scaling = workload_name(args.workload, n)
+    plan = load_plan(name)
+
+    from paper_2509_14098_b200 import executor, run_plan
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        res = run_plan(plan)
+    del res
+    barrier()
+
+    # timed region: K full circuits, device-timed with CUDA events
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    compute_s, launches = 0.0, 0
+    with ClockSampler(local) as clk:
+        barrier()
+        start.record()
+        for _ in range(args.steps):
+            res = run_plan(plan)
+            compute_s += res.stats.compute_seconds
+            launches += res.stats.kernel_launches
+        stop.record()
+        barrier()
+    elapsed = max_over_ranks(start.elapsed_time(stop) / 1e3)
+    compute_s = max_over_ranks(compute_s)
+    stats = res.stats
+    del res
+
+    total_bytes = plan_bytes(plan)
+    value = total_bytes * args.steps / elapsed / 1e9
+    peak, peak_kind = peak_hbm()
+    rows = (1 << plan.g) // world
+    fused = sum(1 for t in plan.tasks if t.kind == "ApplyFused")
+    per_rank_sweep_bytes = fused * 32 * (rows << (plan.d - plan.g))
+    achieved = per_rank_sweep_bytes * args.steps / compute_s / 1e9
+
+    # e2e: initial state from pinned host memory, final blocks back to pinned host
+    torch.cuda.synchronize()
+    d = plan.d
+    e2e = None
+    if (16 << d) <= 40 << 30:
+        host_in = torch.zeros(1 << d, dtype=torch.complex128).pin_memory()
+        host_in[0] = 1.0
+        L = d - plan.g
+        host_out = torch.empty((rows, 1 << L), dtype=torch.complex128).pin_memory()
+        run_plan(plan, initial=host_in)  # warm
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            r = run_plan(plan, initial=host_in)
+            host_out.copy_(r.state.blocks, non_blocking=True)
+            torch.cuda.synchronize()
+            del r
+        barrier()
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
+        e2e = {"value": total_bytes / e2e_s / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 16 << d, "d2h_bytes_per_step": 16 * (rows << L),
+               "ms_per_step": 1e3 * e2e_s}
+
+    traffic = None
+    prof = ROOT / "profiles" / "traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(name)
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": name, "qubits": plan.d, "ranks": 1 << plan.g,
+                   "hierarchy": [plan.d - plan.g, 12], "apply_fused": fused,
+                   "exchanges": [len(t.payload["swaps"]) for t in plan.tasks if t.kind == "Exchange"],
+                   "parallelism": f"state-vector sharding over {n} GPU(s)",
+                   "l2": f"state {16 << plan.d >> 30} GiB >> 126 MB L2 (no flush needed)"},
+        "circuit_ms": 1e3 * elapsed / args.steps,
+        "gates_per_s": sum(len(t.payload["gates"]) for t in plan.tasks if t.kind == "ApplyFused")
+                        * args.steps / elapsed,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_sweep", "peak_source": f"{peak_kind} hbm_gbs",
+                     "bytes_per_launch": 32 * (rows << (plan.d - plan.g)),
+                     "launch_ms": 1e3 * compute_s / (fused * args.steps)},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "compile_ms": 1e3 * stats.compile_seconds,
+        "exchange_ms": 1e3 * stats.exchange_seconds,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline_line()
+        except Exception as e:  # the baseline is reported, never required
+            line["cpu_baseline"] = {"value": None, "error": repr(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

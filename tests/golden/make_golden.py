@@ -200,13 +200,19 @@ BENCH = [
     ("qft24_h22-12", lambda: workloads.qft(24), [22, 12]),
     ("qft26_h23-12", lambda: workloads.qft(26), [23, 12]),
     ("qv20_h18-12", lambda: workloads.quantum_volume(20, seed=20), [18, 12]),
+    ("qft22_h22-12", lambda: workloads.qft(22), [22, 12]),
+    ("qft23_h23-12", lambda: workloads.qft(23), [23, 12]),
+    ("qv22_h22-12", lambda: workloads.quantum_volume(22, seed=22), [22, 12]),
 ]
 
 
-def make_plans(out: Path) -> None:
+def make_plans(out: Path, force: bool = False) -> None:
     out.mkdir(exist_ok=True)
-    meta = {}
+    mpath = out / "plans.json"
+    meta = json.loads(mpath.read_text()) if mpath.exists() and not force else {}
     for name, gen, budgets in BENCH:
+        if name in meta and (out / f"{name}.json.gz").exists():
+            continue
         src = gen()
         t0 = time.perf_counter()
         plan = plan_of(src, budgets)
@@ -228,10 +234,11 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--plans", action="store_true", help="also write benchmark plans to plans/")
     ap.add_argument("--only-plans", action="store_true")
+    ap.add_argument("--force", action="store_true", help="regenerate existing plans")
     a = ap.parse_args()
     if not a.only_plans:
         (HERE / "gates.json").write_text(json.dumps(gates_doc(), indent=1, sort_keys=True) + "\n")
         make_grid(HERE)
         make_cfg1(HERE)
     if a.plans or a.only_plans:
-        make_plans(ROOT / "plans")
+        make_plans(ROOT / "plans", a.force)
