@@ -271,14 +271,25 @@ def _tile_bits_needed(prim) -> set:
     return set()
 
 
-def plan_sweeps(prims: list, geo: DeviceGeometry, kmax: int = KMAX) -> list:
-    """Split a leaf's primitive ops into sweeps whose dense bits fit a tile."""
+LOW_RUN_BITS = 4  # every tile spans device bits 0..3: 256 B contiguous runs
+
+
+def plan_sweeps(prims: list, geo: DeviceGeometry, kmax: int = KMAX, low_bits: int = LOW_RUN_BITS) -> list:
+    """Split a leaf's primitive ops into sweeps whose tiles fit in shared memory.
+
+    Every tile contains the `low_bits` lowest device bits, so each global
+    access is a contiguous run of 2^low_bits amplitudes (the memory system
+    is request-rate bound: 16 B runs reach ~9% of the 256 B-run bandwidth,
+    tools/sweep_membench.py); the rest of the tile holds the leaf's dense
+    target bits, greedily in gate order.
+    """
     D = geo.D
     K = min(kmax, D)
+    low = set(range(min(low_bits, K)))
     groups, cur, need = [], [], set()
     for pr in prims:
         nb = _tile_bits_needed(pr)
-        if len(need | nb) > K and cur:
+        if len(need | nb | low) > K and cur:
             groups.append((cur, need))
             cur, need = [], set()
         cur.append(pr)
@@ -287,8 +298,8 @@ def plan_sweeps(prims: list, geo: DeviceGeometry, kmax: int = KMAX) -> list:
         groups.append((cur, need))
     out = []
     for ops, need in groups:
-        tile = set(need)
-        for b in range(D):  # pad with the lowest device bits (coalescing)
+        tile = set(need) | low
+        for b in range(D):  # pad with the next lowest device bits
             if len(tile) >= K:
                 break
             tile.add(b)
