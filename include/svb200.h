@@ -177,6 +177,23 @@ size_t svb_compare_scratch_bytes(int64_t n);
 int svb_compare(const svb_c128* a, const svb_c128* b, int64_t n, double* out,
                 void* scratch, void* stream);
 
+/* ------------------------------------------------------------------------
+ * 5. Run-time specialised sweep kernels (paper_2509_14098_b200/jit.py).
+ *
+ * svb_jit_compile: NVRTC-compile CUDA source for sm_100a into a cubin
+ *   (malloc'd, release with svb_jit_free); `log` receives the compiler log.
+ * svb_jit_load: load a cubin and return a launchable kernel handle.
+ * svb_jit_launch_sweep: launch a generated sweep kernel on one sweep
+ *   descriptor (same program blob and descriptor as svb_run_sweeps).
+ * ---------------------------------------------------------------------- */
+int svb_jit_compile(const char* src, const char* name, int nopts, const char** opts,
+                    void** image, size_t* size, char* log, size_t logcap);
+void svb_jit_free(void* image);
+int svb_jit_load(const void* image, const char* kernel_name, void** kernel);
+int svb_jit_launch_sweep(void* kernel, svb_c128* state, const void* prog,
+                         const svb_sweep_desc* desc, double* norm_out, int grid_limit,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,7 +20,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 LIB = PKG / "libsvb200.so"
-SOURCES = ["gate_kernels.cu", "sweep.cu", "layout.cu", "reduce.cu"]
+SOURCES = ["gate_kernels.cu", "sweep.cu", "layout.cu", "reduce.cu", "jit.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -35,7 +35,7 @@ def _stale() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + [INCLUDE / "svb200.h"]
+    deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("common.cuh")) + [INCLUDE / "svb200.h"]
     return any(p.stat().st_mtime > t for p in deps if p.exists())
 
 
@@ -62,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             sys.stderr.write(r.stderr)
         objs.append(str(obj))
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart"]
+    cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stderr}")

@@ -1,0 +1,56 @@
+// Device helpers for NVRTC-generated sweep kernels (see jit.py).  Self
+// contained: NVRTC compiles it without the CUDA runtime headers.
+#pragma once
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+struct svb_cterm {
+  int dst;
+  int pad;
+  u64 mask;
+  double re, im;
+};
+
+#define SVB_F __device__ __forceinline__
+
+SVB_F double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * (cr + i ci) with literal parts
+SVB_F double2 cmulc(double2 a, double cr, double ci) {
+  return make_double2(fma(a.x, cr, -a.y * ci), fma(a.x, ci, a.y * cr));
+}
+SVB_F double2 cmulr(double2 a, double cr) { return make_double2(a.x * cr, a.y * cr); }
+// acc + a * (cr + i ci)
+SVB_F double2 cfmac(double2 a, double cr, double ci, double2 acc) {
+  return make_double2(fma(a.x, cr, fma(-a.y, ci, acc.x)), fma(a.x, ci, fma(a.y, cr, acc.y)));
+}
+SVB_F double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+SVB_F double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+SVB_F void cp_async16(double2* smem_dst, const double2* gmem_src) {
+  const u32 sa = (u32)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem_src) : "memory");
+}
+SVB_F void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+SVB_F void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+SVB_F void st_stream(double2* p, double2 v) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// per-tile phase slots: slot i is computed by thread (i % nw) * 32 + i / nw
+// so the work spreads over the warps of the CTA
+SVB_F void tile_slots(double2* ctab, int nct, const svb_cterm* __restrict__ cterms,
+                      const int* __restrict__ cofs, u64 base, int t, int nthreads) {
+  const int nw = nthreads >> 5;
+  const int first = nw ? (t >> 5) + nw * (t & 31) : t;
+  for (int i = first; i < nct; i += nthreads) {
+    double2 acc = make_double2(1.0, 0.0);
+    for (int q = cofs[i]; q < cofs[i + 1]; ++q) {
+      const svb_cterm c = cterms[q];
+      if ((base & c.mask) == c.mask) acc = cmul(acc, make_double2(c.re, c.im));
+    }
+    ctab[i] = acc;
+  }
+}

@@ -21,6 +21,7 @@ There is no CPU execution path: without the CUDA library every call raises.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -91,6 +92,18 @@ def _dist_info(group=None):
     return 0, 1
 
 
+JIT_MIN_D = int(os.environ.get("SVB200_JIT_MIN_D", "16"))
+
+
+def _use_jit(geo: prog.DeviceGeometry, jit) -> bool:
+    if jit is not None:
+        return bool(jit)
+    env = os.environ.get("SVB200_JIT")
+    if env is not None:
+        return env not in ("0", "false", "no")
+    return geo.D >= JIT_MIN_D
+
+
 @dataclass
 class _Compiled:
     blob: torch.Tensor
@@ -99,16 +112,19 @@ class _Compiled:
     n_fused: int
     compile_seconds: float
     host_blob: np.ndarray = field(repr=False, default=None)
+    kernels: list | None = None  # per-descriptor JIT kernel handles (None: interpreter)
+    jit_seconds: float = 0.0
 
 
 _compile_cache: dict = {}
 
 
-def compile_plan(plan, geo: prog.DeviceGeometry, device) -> _Compiled:
+def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None) -> _Compiled:
     """Compile every ApplyFused task of the plan for this device (cached)."""
     import time
 
-    key = (id(plan), len(plan.tasks), geo.d, geo.g, geo.h, geo.rank_base, str(device))
+    use_jit = _use_jit(geo, jit)
+    key = (id(plan), len(plan.tasks), geo.d, geo.g, geo.h, geo.rank_base, str(device), use_jit)
     hit = _compile_cache.get(key)
     if hit is not None and hit[0] is plan:
         return hit[1]
@@ -128,6 +144,14 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device) -> _Compiled:
     host = np.ascontiguousarray(blob)
     dev_blob = torch.from_numpy(host).to(device)
     out = _Compiled(dev_blob, descs, task_sweeps, slot, time.perf_counter() - t0, host)
+    if use_jit and buf.descs:
+        from . import jit as jitmod
+
+        t1 = time.perf_counter()
+        names, cubins = jitmod.build_kernels(buf)
+        dev_index = device.index if device.index is not None else torch.cuda.current_device()
+        out.kernels = [jitmod.load_kernel(n, c, dev_index) for n, c in zip(names, cubins)]
+        out.jit_seconds = time.perf_counter() - t1
     _compile_cache.clear()  # keep one plan resident
     _compile_cache[key] = (plan, out)
     return out
@@ -171,7 +195,7 @@ class _State:
 
 
 def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=None, *,
-             device=None, group=None, grid_limit: int = 0) -> RunResult:
+             device=None, group=None, grid_limit: int = 0, jit=None) -> RunResult:
     """Interpret the task list on the GPU(s); returns the final state and optional histogram.
 
     Same contract as ``svpart.executor.run_plan`` (executor.py:179-307).
@@ -247,20 +271,27 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 full = scatter(initial, plan, phase=0, device=device)
                 state.blocks.copy_(full.blocks[rank_base:rank_base + rows])
                 del full
-            compiled = compile_plan(plan, geo_eff, device)
-            stats.compile_seconds = compiled.compile_seconds
+            compiled = compile_plan(plan, geo_eff, device, jit)
+            stats.compile_seconds = compiled.compile_seconds + compiled.jit_seconds
             norms = torch.zeros(max(compiled.n_fused, 1), dtype=torch.float64, device=device)
         elif kind == "ApplyFused":
             if state is None:
                 fail(PlanInvalid("compute before Alloc"))
             first, count, _slot = compiled.task_sweeps[task.id]
             descs = compiled.descs[first:first + count]
-            rc = lib.svb_run_sweeps(
-                state.buf.data_ptr(), rows_eff, L,
-                compiled.blob.data_ptr(), descs.ctypes.data, count, norms.data_ptr(), grid_limit,
-                stream,
-            )
-            _native.check(rc, "svb_run_sweeps")
+            if compiled.kernels is None:
+                rc = lib.svb_run_sweeps(
+                    state.buf.data_ptr(), rows_eff, L, compiled.blob.data_ptr(), descs.ctypes.data,
+                    count, norms.data_ptr(), grid_limit, stream,
+                )
+                _native.check(rc, "svb_run_sweeps")
+            else:
+                for i in range(count):
+                    rc = lib.svb_jit_launch_sweep(
+                        compiled.kernels[first + i], state.buf.data_ptr(), compiled.blob.data_ptr(),
+                        descs[i:i + 1].ctypes.data, norms.data_ptr(), grid_limit, stream,
+                    )
+                    _native.check(rc, "svb_jit_launch_sweep")
             stats.sweeps += count
             stats.kernel_launches += count
             fused_order.append(task.id)

@@ -1,0 +1,405 @@
+"""Render compiled sweeps as straight-line CUDA and build them with NVRTC.
+
+The generic sweep kernel (csrc/sweep.cu) interprets a short op list per
+tile; on large states the interpretation overhead (op dispatch, register
+moves between templated cases, runtime index math) dominates the FP64 work
+(ncu: ~6,600 warp instructions per 4096-amplitude tile, ~1,550 of them
+FP64).  Here each sweep becomes its own kernel: register slots, control
+masks, smem swizzle offsets and gate coefficients are compile-time
+constants, so what remains is the arithmetic plus one load and one store
+per amplitude.  This is the reference paper's code-generation step (a
+kernel per partition, section 4) performed at run time.
+
+Kernels are compiled in parallel (NVRTC releases the GIL through ctypes)
+and cached by source hash in memory and on disk.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import os
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+import numpy as np
+
+from . import _native
+from . import program as prog
+
+CSRC = Path(__file__).resolve().parent / "csrc"
+CACHE_DIR = Path(os.environ.get("SVB200_JIT_CACHE", Path(__file__).resolve().parent.parent / "build" / "jit_cache"))
+NVRTC_OPTS = ["--gpu-architecture=sm_100a", "--std=c++17", f"-I{CSRC}", "-lineinfo",
+              "--extra-device-vectorization"]
+
+RB, NR = prog.RB, prog.NREG
+
+
+# ---------------------------------------------------------------------------
+# expression helpers
+# ---------------------------------------------------------------------------
+
+def _lit(x: float) -> str:
+    r = repr(float(x))
+    return r if ("e" in r or "." in r or "inf" in r or "nan" in r) else r + ".0"
+
+
+def _cmul_lit(expr: str, c: complex) -> str:
+    cr, ci = float(c.real), float(c.imag)
+    if ci == 0.0:
+        if cr == 1.0:
+            return expr
+        if cr == -1.0:
+            return f"make_double2(-({expr}).x, -({expr}).y)"
+        return f"cmulr({expr}, {_lit(cr)})"
+    if cr == 0.0:
+        return f"make_double2(-({expr}).y * {_lit(ci)}, ({expr}).x * {_lit(ci)})"
+    return f"cmulc({expr}, {_lit(cr)}, {_lit(ci)})"
+
+
+def _lincomb(terms) -> str:
+    """sum_k c_k * x_k for literal complex c_k (drops zero terms)."""
+    terms = [(c, x) for c, x in terms if c != 0]
+    if not terms:
+        return "make_double2(0.0, 0.0)"
+    c0, x0 = terms[0]
+    acc = _cmul_lit(x0, c0)
+    for c, x in terms[1:]:
+        cr, ci = float(c.real), float(c.imag)
+        if ci == 0.0 and cr == 1.0:
+            acc = f"cadd({acc}, {x})"
+        elif ci == 0.0 and cr == -1.0:
+            acc = f"csub({acc}, {x})"
+        else:
+            acc = f"cfmac({x}, {_lit(cr)}, {_lit(ci)}, {acc})"
+    return acc
+
+
+def _deposit(var: str, dst_bits) -> str:
+    """Expression placing bit i of `var` at position dst_bits[i] (runs merged)."""
+    parts, i, n = [], 0, len(dst_bits)
+    while i < n:
+        j = i
+        while j + 1 < n and dst_bits[j + 1] == dst_bits[j] + 1:
+            j += 1
+        width = j - i + 1
+        mask = (1 << width) - 1
+        shift = dst_bits[i] - i
+        src = f"(((u64){var} >> {i}) & {mask}ull)"
+        parts.append(f"({src} << {shift})" if shift > 0 else src)
+        i = j + 1
+    return " | ".join(parts) if parts else "0ull"
+
+
+def _xor_img(var: str, imgs) -> str:
+    parts = [f"((({var}) >> {i}) & 1u ? {int(s)}u : 0u)" for i, s in enumerate(imgs) if s]
+    return " ^ ".join(parts) if parts else "0u"
+
+
+# ---------------------------------------------------------------------------
+# kernel generator
+# ---------------------------------------------------------------------------
+
+def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
+    K, D = desc["K"], desc["D"]
+    NT = 1 << (K - RB)
+    tin = list(desc["tin"])[:K]
+    sw = list(desc["sw"])[:K]
+    st_dev = list(desc["st_dev"])[:K]
+    st_sw = list(desc["st_sw"])[:K]
+    st_flip = int(desc["st_flip"])
+    nct = int(desc["nctab"])
+    fbits = [b for b in range(D) if b not in tin]
+    ntiles = 1 << (D - K)
+    tb = K - RB  # thread bits
+
+    L = []
+    w = L.append
+    w('#include "sweep_jit.cuh"')
+    w(f'extern "C" __global__ void __launch_bounds__({NT}, 1)')
+    w(f"{name}(double2* __restrict__ state, const double2* __restrict__ tab, "
+      "const svb_cterm* __restrict__ cterms, const int* __restrict__ cofs, double* __restrict__ norm_out) {")
+    w("  extern __shared__ __align__(16) double2 smem[];")
+    w("  __shared__ double red[32];")
+    w("  const int t = threadIdx.x;")
+    w(f"  double2* const ctab = smem + {2 << K};")
+    # per-thread constants
+    w(f"  const u64 ld_t = {_deposit('t', tin[:tb])};")
+    w(f"  const u32 lds_t = {_xor_img('t', sw[:tb])};")
+    w(f"  const u64 st_t = {_deposit('t', st_dev[:tb])};")
+    w(f"  const u32 sts_t = {_xor_img('t', st_sw[:tb])};")
+    stages = [op for op in ops if op["kind"] == prog.OP_STAGE]
+    stage_info = []
+    for si, st in enumerate(stages):
+        rm = int(st["rmask"])
+        regs = [k for k in range(K) if (rm >> k) & 1]
+        comp = [k for k in range(K) if not (rm >> k) & 1]
+        w(f"  const u32 sb{si} = {_xor_img('t', [sw[k] for k in comp])};")
+        w(f"  const u64 db{si} = {_deposit('t', [tin[k] for k in comp])};")
+        offs = []
+        for v in range(NR):
+            o = 0
+            for q in range(RB):
+                if (v >> q) & 1:
+                    o ^= sw[regs[q]]
+            offs.append(o)
+        stage_info.append((regs, comp, offs))
+    w("  double nrm = 0.0;")
+    w(f"  long long tile_id = blockIdx.x;")
+
+    def origin(var):
+        return _deposit(var, fbits) if fbits else "0ull"
+
+    def prefetch(buf, base):
+        w("    {")
+        for it in range(NR):
+            dev = 0
+            s = 0
+            for q in range(RB):
+                if (it >> q) & 1:
+                    dev |= 1 << tin[tb + q]
+                    s ^= sw[tb + q]
+            w(f"      cp_async16({buf} + (lds_t ^ {s}u), state + ({base} | ld_t | {dev}ull));")
+        w("      cp_async_commit();")
+        w("    }")
+
+    w(f"  if (tile_id < {ntiles}ll) {{")
+    w(f"    const u64 b0 = {origin('tile_id')};")
+    prefetch("smem", "b0")
+    w("  }")
+    w(f"  for (int iter = 0; tile_id < {ntiles}ll; ++iter, tile_id += gridDim.x) {{")
+    w(f"    double2* const tile = (iter & 1) ? smem + {1 << K} : smem;")
+    w(f"    const u64 base = {origin('tile_id')};")
+    if nct:
+        w(f"    tile_slots(ctab, {nct}, cterms, cofs, base, t, {NT});")
+    w("    cp_async_wait_all();")
+    w("    __syncthreads();")
+    w(f"    if (tile_id + gridDim.x < {ntiles}ll) {{")
+    w("      const long long nx = tile_id + gridDim.x;")
+    w(f"      const u64 bn = {origin('nx')};")
+    w(f"      double2* const nbuf = (iter & 1) ? smem : smem + {1 << K};")
+    prefetch("nbuf", "bn")
+    w("    }")
+    w("    double2 x[16];")
+
+    cur = None  # current stage index
+    for op in ops:
+        kind = int(op["kind"])
+        if kind == prog.OP_STAGE:
+            nxt = 0 if cur is None else cur + 1
+            if cur is not None:
+                _, _, offs = stage_info[cur]
+                for v in range(NR):
+                    w(f"    tile[sb{cur} ^ {offs[v]}u] = x[{v}];")
+                w("    __syncthreads();")
+            _, _, offs = stage_info[nxt]
+            for v in range(NR):
+                w(f"    x[{v}] = tile[sb{nxt} ^ {offs[v]}u];")
+            cur = nxt
+            continue
+        _emit_op(w, op, coef, cur, K)
+
+    if cur is not None:
+        _, _, offs = stage_info[cur]
+        for v in range(NR):
+            w(f"    tile[sb{cur} ^ {offs[v]}u] = x[{v}];")
+    w("    __syncthreads();")
+    for it in range(NR):
+        dev = 0
+        s = 0
+        for q in range(RB):
+            if (it >> q) & 1:
+                dev |= 1 << st_dev[tb + q]
+                s ^= st_sw[tb + q]
+        w("    {")
+        w(f"      const double2 v = tile[sts_t ^ {s}u];")
+        w("      nrm = fma(v.x, v.x, fma(v.y, v.y, nrm));")
+        w(f"      st_stream(state + (base | ((st_t | {dev}ull) ^ {st_flip}ull)), v);")
+        w("    }")
+    w("  }")
+    w("  cp_async_wait_all();")
+    w("  if (norm_out != nullptr) {")
+    full = "0xffffffffu" if NT >= 32 else f"{(1 << NT) - 1}u"
+    for o in (16, 8, 4, 2, 1):
+        if o < NT:
+            w(f"    nrm += __shfl_xor_sync({full}, nrm, {o});")
+    w("    if ((t & 31) == 0) red[t >> 5] = nrm;")
+    w("    __syncthreads();")
+    w("    if (t == 0) {")
+    w("      double s = 0.0;")
+    w(f"      for (int i = 0; i < {(NT + 31) // 32}; ++i) s += red[i];")
+    w("      atomicAdd(norm_out, s);")
+    w("    }")
+    w("  }")
+    w("}")
+    return "\n".join(L) + "\n"
+
+
+def _phase_base(w, op, coef_c0: complex, K: int) -> None:
+    """Emit `p` = const * per-tile slot * per-thread table * per-thread-bit slots."""
+    w(f"      double2 p = make_double2({_lit(coef_c0.real)}, {_lit(coef_c0.imag)});")
+    if int(op["ctab"]) >= 0:
+        w(f"      p = cmul(p, ctab[{int(op['ctab'])}]);")
+    if int(op["tab"]) >= 0:
+        w(f"      p = cmul(p, __ldg(tab + {int(op['tab'])} + t));")
+    if int(op["tf"]) >= 0:
+        for i in range(K - RB):
+            w(f"      if ((t >> {i}) & 1) p = cmul(p, ctab[{int(op['tf']) + i}]);")
+
+
+def _emit_op(w, op, coef, stage, K) -> None:
+    kind = int(op["kind"])
+    a = int(op["a"])
+    A = 1 << a
+    cm, cv = int(op["rmask"]), int(op["b"])
+    cf = int(op["coef"])
+    pmask, pval = int(op["pmask"]), int(op["pval"])
+    w("    {")
+    if pmask:
+        w(f"    if (((base | db{stage}) & {pmask}ull) == {pval}ull) {{")
+    if kind in (prog.OP_H, prog.OP_U1, prog.OP_PH):
+        has_phase = kind == prog.OP_PH or (int(op["flags"]) & prog.F_PHASE)
+        fused = False
+        if has_phase:
+            ph = cf if kind == prog.OP_PH else cf + 4
+            _phase_base(w, op, coef[ph], K)
+            nt = (int(op["flags"]) >> prog.F_PREG_SHIFT) & 0xF
+            fused = kind == prog.OP_H and cm == 0
+            _emit_dfs(w, a, nt, [coef[ph + 1 + s] for s in range(RB)], fused)
+        if kind == prog.OP_H and not fused:
+            for v in range(NR):
+                if (v & A) or (v & cm) != cv:
+                    continue
+                w(f"      {{ const double2 x0 = x[{v}], x1 = x[{v | A}]; "
+                  f"x[{v}] = cadd(x0, x1); x[{v | A}] = csub(x0, x1); }}")
+        elif kind == prog.OP_U1:
+            m00, m01, m10, m11 = coef[cf:cf + 4]
+            for v in range(NR):
+                if (v & A) or (v & cm) != cv:
+                    continue
+                w(f"      {{ const double2 x0 = x[{v}], x1 = x[{v | A}]; "
+                  f"x[{v}] = {_lincomb([(m00, 'x0'), (m01, 'x1')])}; "
+                  f"x[{v | A}] = {_lincomb([(m10, 'x0'), (m11, 'x1')])}; }}")
+    elif kind == prog.OP_X:
+        for v in range(NR):
+            if (v & A) or (v & cm) != cv:
+                continue
+            w(f"      {{ const double2 tmp = x[{v}]; x[{v}] = x[{v | A}]; x[{v | A}] = tmp; }}")
+    elif kind == prog.OP_U2:
+        b = int(op["b"])
+        B = 1 << b
+        M = np.asarray(coef[cf:cf + 16]).reshape(4, 4)
+        for v in range(NR):
+            if (v & A) or (v & B):
+                continue
+            idx = [v, v | B, v | A, v | A | B]
+            w("      {")
+            w(f"        const double2 a0 = x[{idx[0]}], a1 = x[{idx[1]}], a2 = x[{idx[2]}], a3 = x[{idx[3]}];")
+            for r in range(4):
+                w(f"        x[{idx[r]}] = {_lincomb([(M[r, c], f'a{c}') for c in range(4)])};")
+            w("      }")
+    elif kind == prog.OP_PHALL:
+        _phase_base(w, op, coef[cf], K)
+        for v in range(NR):
+            w(f"      x[{v}] = cmul(x[{v}], p);")
+    elif kind == prog.OP_SCALE:
+        for v in range(NR):
+            w(f"      x[{v}] = {_cmul_lit(f'x[{v}]', coef[cf])};")
+    if pmask:
+        w("    }")
+    w("    }")
+
+
+def _emit_dfs(w, a: int, nt: int, c: list, fused_h: bool) -> None:
+    """Depth-first product over register slots != a; leaves are amplitudes with bit a set."""
+    counter = [0]
+
+    def rec(s, v, pv):
+        if s == RB:
+            if fused_h:
+                w(f"      {{ const double2 x1 = cmul(x[{v}], {pv}); const double2 x0 = x[{v ^ (1 << a)}]; "
+                  f"x[{v ^ (1 << a)}] = cadd(x0, x1); x[{v}] = csub(x0, x1); }}")
+            else:
+                w(f"      x[{v}] = cmul(x[{v}], {pv});")
+            return
+        if s == a:
+            rec(s + 1, v, pv)
+            return
+        rec(s + 1, v, pv)
+        if (nt >> s) & 1:
+            counter[0] += 1
+            q = f"q{counter[0]}"
+            w(f"      const double2 {q} = {_cmul_lit(pv, c[s])};")
+            rec(s + 1, v | (1 << s), q)
+        else:
+            rec(s + 1, v | (1 << s), pv)
+
+    rec(0, 1 << a, "p")
+
+
+# ---------------------------------------------------------------------------
+# compile / load / launch
+# ---------------------------------------------------------------------------
+
+_mem_cache: dict = {}  # source hash -> cubin bytes
+_kernels: dict = {}  # (source hash, device) -> kernel handle
+
+
+def _compile(src: str, name: str) -> bytes:
+    h = hashlib.sha256((src + "\0" + " ".join(NVRTC_OPTS)).encode()).hexdigest()
+    hit = _mem_cache.get(h)
+    if hit is not None:
+        return hit
+    path = CACHE_DIR / f"{h}.cubin"
+    if path.exists():
+        data = path.read_bytes()
+        _mem_cache[h] = data
+        return data
+    lib = _native.load()
+    opts = (ctypes.c_char_p * len(NVRTC_OPTS))(*[o.encode() for o in NVRTC_OPTS])
+    image = ctypes.c_void_p()
+    size = ctypes.c_size_t()
+    log = ctypes.create_string_buffer(1 << 16)
+    rc = lib.svb_jit_compile(src.encode(), name.encode(), len(NVRTC_OPTS), opts, ctypes.byref(image),
+                             ctypes.byref(size), log, len(log))
+    if rc != 0:
+        raise _native.NativeError(f"NVRTC failed for {name}: {log.value.decode(errors='replace')[:4000]}")
+    data = ctypes.string_at(image, size.value)
+    lib.svb_jit_free(image)
+    try:
+        CACHE_DIR.mkdir(parents=True, exist_ok=True)
+        tmp = path.with_suffix(f".tmp{os.getpid()}")
+        tmp.write_bytes(data)
+        os.replace(tmp, path)
+    except OSError:
+        pass
+    _mem_cache[h] = data
+    return data
+
+
+def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: int | None = None):
+    """Generate + compile one kernel per sweep descriptor; returns (names, cubins, hashes)."""
+    srcs, names = [], []
+    for i, d in enumerate(buf.descs):
+        ops = buf.ops[d["op_begin"]: d["op_begin"] + d["op_count"]]
+        body = kernel_source("KNAME", d, ops, buf.coef)
+        h = hashlib.sha1(body.encode()).hexdigest()[:16]
+        name = f"{prefix}_{h}"
+        srcs.append(body.replace("KNAME", name))
+        names.append(name)
+    threads = threads or min(32, os.cpu_count() or 4)
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        cubins = list(ex.map(lambda sn: _compile(*sn), zip(srcs, names)))
+    return names, cubins
+
+
+def load_kernel(name: str, cubin: bytes, device_index: int):
+    key = (name, device_index)
+    k = _kernels.get(key)
+    if k is None:
+        lib = _native.load()
+        handle = ctypes.c_void_p()
+        _native.check(lib.svb_jit_load(cubin, name.encode(), ctypes.byref(handle)), "svb_jit_load")
+        k = handle.value
+        _kernels[key] = k
+    return k

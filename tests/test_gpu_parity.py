@@ -69,3 +69,25 @@ def test_cfg1_qft20_four_ranks(cfg1_docs, cfg1_fp, key):
     assert np.max(np.abs(flat[idx] - cfg1_fp[key + "::amps"])) < TOL
     assert abs(flat.sum() - cfg1_fp[key + "::sum"][0]) < 1e-8
     assert res.state.layouts == cfg1_docs[key]["plan"]["layout_phases"]
+
+
+def test_grid_jit_path_matches_reference(grid_docs, grid_states):
+    """The NVRTC-specialised kernels on a slice of the grid (both code paths are product paths)."""
+    n = 0
+    for doc in grid_docs:
+        name = doc["name"]
+        if name not in grid_states or doc["plan"]["d"] < 8 or n >= 60:
+            continue
+        res = _run(plan_from_doc(doc["plan"]), jit=True)
+        err = float(np.max(np.abs(res.state.blocks.cpu().numpy() - grid_states[name])))
+        assert err < TOL, (name, err)
+        n += 1
+    assert n == 60
+
+
+@pytest.mark.parametrize("key", ["18", "18_12"])
+def test_cfg1_interpreter_path(cfg1_docs, cfg1_fp, key):
+    plan = plan_from_doc(cfg1_docs[key]["plan"])
+    flat = _run(plan, jit=False).state.blocks.reshape(-1).cpu().numpy()
+    idx = cfg1_fp[key + "::idx"]
+    assert np.max(np.abs(flat[idx] - cfg1_fp[key + "::amps"])) < TOL
