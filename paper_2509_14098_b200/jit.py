@@ -84,7 +84,7 @@ def _deposit(var: str, dst_bits) -> str:
             j += 1
         width = j - i + 1
         mask = (1 << width) - 1
-        shift = dst_bits[i] - i
+        shift = dst_bits[i]
         src = f"(((u64){var} >> {i}) & {mask}ull)"
         parts.append(f"({src} << {shift})" if shift > 0 else src)
         i = j + 1
