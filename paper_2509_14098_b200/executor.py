@@ -57,6 +57,7 @@ class RunStats:
     compile_seconds: float = 0.0
     sweeps: int = 0
     kernel_launches: int = 0
+    layout_seconds: float = 0.0  # trailing sweeps restoring the reference layout
 
 
 @dataclass
@@ -108,12 +109,14 @@ def _use_jit(geo: prog.DeviceGeometry, jit) -> bool:
 class _Compiled:
     blob: torch.Tensor
     descs: np.ndarray
-    task_sweeps: dict  # task id -> (first desc, count)
+    steps: dict  # task id -> prog.Step; None -> trailing materialization step
+    init_perm: list  # reference device bit -> physical bit at Alloc
     n_fused: int
     compile_seconds: float
     host_blob: np.ndarray = field(repr=False, default=None)
     kernels: list | None = None  # per-descriptor JIT kernel handles (None: interpreter)
     jit_seconds: float = 0.0
+    n_sweeps: int = 0
 
 
 _compile_cache: dict = {}
@@ -129,26 +132,20 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None) -> _Compiled:
     if hit is not None and hit[0] is plan:
         return hit[1]
     t0 = time.perf_counter()
-    buf = prog.ProgramBuffers()
-    task_sweeps = {}
-    slot = 0
-    for task in plan.tasks:
-        if task.kind != "ApplyFused":
-            continue
-        layout = plan.layout_phases[task.payload["phase"]]
-        first = len(buf.descs)
-        n = prog.compile_leaf(task.payload, layout, geo, slot, buf)
-        task_sweeps[task.id] = (first, n, slot)
-        slot += 1
-    blob, descs, _ = prog.pack(buf)
+    dp = prog.plan_device(plan, geo)
+    blob, descs, _ = prog.pack(dp.buf)
     host = np.ascontiguousarray(blob)
     dev_blob = torch.from_numpy(host).to(device)
-    out = _Compiled(dev_blob, descs, task_sweeps, slot, time.perf_counter() - t0, host)
-    if use_jit and buf.descs:
+    steps = {}
+    for st in dp.steps:
+        steps[st.task_id] = st
+    out = _Compiled(dev_blob, descs, steps, dp.init_perm, dp.n_fused, time.perf_counter() - t0,
+                    host, n_sweeps=len(dp.buf.descs))
+    if use_jit and dp.buf.descs:
         from . import jit as jitmod
 
         t1 = time.perf_counter()
-        names, cubins = jitmod.build_kernels(buf)
+        names, cubins = jitmod.build_kernels(dp.buf)
         dev_index = device.index if device.index is not None else torch.cuda.current_device()
         out.kernels = [jitmod.load_kernel(n, c, dev_index) for n, c in zip(names, cubins)]
         out.jit_seconds = time.perf_counter() - t1
@@ -245,8 +242,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
 
             dist.all_reduce(t, group=group)
             vals = t.cpu().numpy()
-        for tid in fused_order:
-            slot = compiled.task_sweeps[tid][2]
+        for slot, tid in enumerate(fused_order):
             nv = float(vals[slot])
             if abs(nv - 1.0) > DRIFT_TOL:
                 raise NonUnitaryDrift(f"norm drifted to {nv!r}")
@@ -264,34 +260,22 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             if task.payload["num_ranks"] != nranks or task.payload["block_len"] != 1 << L:
                 fail(PlanInvalid("Alloc payload disagrees with plan shape"))
             state = _State(rows, L, device)
-            if initial is None:
-                if rank_base == 0:
-                    state.blocks[0, 0] = 1.0
-            else:
-                full = scatter(initial, plan, phase=0, device=device)
-                state.blocks.copy_(full.blocks[rank_base:rank_base + rows])
-                del full
             compiled = compile_plan(plan, geo_eff, device, jit)
             stats.compile_seconds = compiled.compile_seconds + compiled.jit_seconds
+            if initial is None:
+                if rank_base == 0:
+                    state.blocks[0, 0] = 1.0  # |0...0> sits at index 0 in every layout
+            else:
+                full = scatter(initial, plan, phase=0, device=device, local_perm=compiled.init_perm[:L])
+                state.blocks.copy_(full.blocks[rank_base:rank_base + rows])
+                del full
             norms = torch.zeros(max(compiled.n_fused, 1), dtype=torch.float64, device=device)
         elif kind == "ApplyFused":
             if state is None:
                 fail(PlanInvalid("compute before Alloc"))
-            first, count, _slot = compiled.task_sweeps[task.id]
-            descs = compiled.descs[first:first + count]
-            if compiled.kernels is None:
-                rc = lib.svb_run_sweeps(
-                    state.buf.data_ptr(), rows_eff, L, compiled.blob.data_ptr(), descs.ctypes.data,
-                    count, norms.data_ptr(), grid_limit, stream,
-                )
-                _native.check(rc, "svb_run_sweeps")
-            else:
-                for i in range(count):
-                    rc = lib.svb_jit_launch_sweep(
-                        compiled.kernels[first + i], state.buf.data_ptr(), compiled.blob.data_ptr(),
-                        descs[i:i + 1].ctypes.data, norms.data_ptr(), grid_limit, stream,
-                    )
-                    _native.check(rc, "svb_jit_launch_sweep")
+            st = compiled.steps[task.id]
+            _run_descs(compiled, st.first, st.count, state, rows_eff, L, norms, grid_limit, stream)
+            count = st.count
             stats.sweeps += count
             stats.kernel_launches += count
             fused_order.append(task.id)
@@ -306,7 +290,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 fail(PlanInvalid("Exchange without matching Pack"))
             swaps = task.payload["swaps"]
             m = len(swaps)
-            launches = _remap(state, swaps, geo, group, stream)
+            launches = _remap(state, compiled.steps[task.id].swaps, geo, group, stream)
             stats.kernel_launches += launches
             moved = nranks * ((1 << m) - 1) * (1 << (L - m))
             messages = nranks * ((1 << m) - 1)
@@ -330,6 +314,15 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
 
     if state is None:
         raise PlanInvalid("plan never allocated state")
+    mat = compiled.steps.get(None)
+    if mat is not None:  # restore the reference layout
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _run_descs(compiled, mat.first, mat.count, state, rows_eff, L, None, grid_limit, stream)
+        e1.record()
+        events.append(("Materialize", e0, e1))
+        stats.sweeps += mat.count
+        stats.kernel_launches += mat.count
     torch.cuda.synchronize(device)
     for kind, e0, e1 in events:
         sec = e0.elapsed_time(e1) / 1e3
@@ -337,6 +330,8 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             stats.exchange_seconds += sec
         elif kind == "ApplyFused":
             stats.compute_seconds += sec
+        elif kind == "Materialize":
+            stats.layout_seconds += sec
     _check_norms()
 
     dstate = DistState(
@@ -350,14 +345,33 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
     return RunResult(state=dstate, histogram=histogram, stats=stats)
 
 
+def _run_descs(compiled, first, count, state, rows_eff, L, norms, grid_limit, stream) -> None:
+    lib = _native.load()
+    if not count:
+        return
+    descs = compiled.descs[first:first + count]
+    nptr = norms.data_ptr() if norms is not None else None
+    if compiled.kernels is None:
+        rc = lib.svb_run_sweeps(state.buf.data_ptr(), rows_eff, L, compiled.blob.data_ptr(),
+                                descs.ctypes.data, count, nptr, grid_limit, stream)
+        _native.check(rc, "svb_run_sweeps")
+        return
+    for i in range(count):
+        rc = lib.svb_jit_launch_sweep(compiled.kernels[first + i], state.buf.data_ptr(),
+                                      compiled.blob.data_ptr(), descs[i:i + 1].ctypes.data, nptr,
+                                      grid_limit, stream)
+        _native.check(rc, "svb_jit_launch_sweep")
+
+
 def _remap(state: _State, swaps: list, geo: prog.DeviceGeometry, group, stream) -> int:
-    """Pairwise bit swaps rank_bit <-> local_bit (executor.py:224-281)."""
+    """Pairwise bit swaps rank bit <-> physical local bit (executor.py:224-281).
+
+    `swaps` are (rank integer bit, physical local device bit) from the schedule.
+    """
     lib = _native.load()
     L, g, h = geo.L, geo.g, geo.h
     local_u, local_w, remote = [], [], []
-    for s in swaps:
-        ib = g - 1 - s["rank_bit"]
-        lb = L - 1 - s["local_bit"]
+    for ib, lb in swaps:
         if ib < h:
             local_u.append(L + ib)
             local_w.append(lb)
@@ -416,8 +430,12 @@ def gather(state: DistState) -> np.ndarray:
     return gather_device(state).cpu().numpy()
 
 
-def scatter(dense, plan, phase: int = 0, device=None) -> DistState:
-    """Distribute a dense state into rank blocks at the given layout phase (executor.py:329-343)."""
+def scatter(dense, plan, phase: int = 0, device=None, local_perm=None) -> DistState:
+    """Distribute a dense state into rank blocks at the given layout phase (executor.py:329-343).
+
+    `local_perm` (internal) additionally places reference local bit r at
+    physical bit local_perm[r] (the executor's initial layout).
+    """
     device = _require_cuda(device)
     d, g = plan.d, plan.g
     shape = tuple(dense.shape)
@@ -432,7 +450,11 @@ def scatter(dense, plan, phase: int = 0, device=None) -> DistState:
     if d == 0:
         flat.copy_(src)
     else:
-        _bitperm(src, flat, _storage_bitperm(layout, d, to_basis=False))
+        perm = _storage_bitperm(layout, d, to_basis=False)
+        if local_perm is not None:
+            L = d - g
+            perm = [local_perm[p] if p < L else p for p in perm]
+        _bitperm(src, flat, perm)
     return DistState(
         blocks=flat.view(1 << g, 1 << (d - g)), phase=phase, d=d, g=g,
         layouts=[list(p) for p in plan.layout_phases],

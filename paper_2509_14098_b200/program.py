@@ -109,6 +109,7 @@ class Dense1:
     bit: int
     m: np.ndarray
     ctrl: dict  # device bit -> required value (0/1)
+    noop: bool = False  # a constant-0 control made it identity on this device
 
 
 @dataclass
@@ -215,7 +216,10 @@ def resolve_entry(entry: dict, layout, geo: DeviceGeometry) -> list:
 
     # non-diagonal: fixed slots are controls (validated above)
     if any(slot_const[i] == 0 for i in fixed):
-        return []  # a constant-0 control: identity on this device
+        # identity on this device; kept as a placeholder so every device plans
+        # the same tiles and layouts
+        tgt = [slot_bit[i] for i in free if i not in gate.controls]
+        return [Dense1(tgt[0], np.eye(2, dtype=np.complex128), {}, noop=True)] if tgt else []
     m = np.asarray(gate.matrix).reshape((2,) * (2 * p))
     idx = [slice(None)] * (2 * p)
     for i in fixed:
@@ -256,64 +260,36 @@ class _Item:
 @dataclass
 class SweepProgram:
     K: int
-    tin: list  # tile-local k -> device bit
+    tin: list  # tile-local k -> physical device bit (sorted)
     items: list
-    out_map: dict  # physical device bit -> (reference device bit, flip)
+    out_map: dict  # physical tile bit -> (destination device bit, flip)
     norm_slot: int = -1
     scale: complex = 1.0
 
 
-def _tile_bits_needed(prim) -> set:
+LOW_RUN_BITS = 4  # every tile spans physical bits 0..3: 256 B contiguous runs
+
+
+def _needs(prim) -> list:
+    """Reference bits a primitive needs inside the tile (dense targets, virtual flips)."""
     if isinstance(prim, Dense1):
-        return {prim.bit}
-    if isinstance(prim, Swap):
-        return {prim.a, prim.b}
-    return set()
+        return [prim.bit]
+    return []
 
 
-LOW_RUN_BITS = 4  # every tile spans device bits 0..3: 256 B contiguous runs
+def build_sweep(prims: list, tile: list, where: list) -> SweepProgram:
+    """Phase scheduling for one sweep.
 
-
-def plan_sweeps(prims: list, geo: DeviceGeometry, kmax: int = KMAX, low_bits: int = LOW_RUN_BITS) -> list:
-    """Split a leaf's primitive ops into sweeps whose tiles fit in shared memory.
-
-    Every tile contains the `low_bits` lowest device bits, so each global
-    access is a contiguous run of 2^low_bits amplitudes (the memory system
-    is request-rate bound: 16 B runs reach ~9% of the 256 B-run bandwidth,
-    tools/sweep_membench.py); the rest of the tile holds the leaf's dense
-    target bits, greedily in gate order.
+    `where` maps reference device bit -> physical device bit for the whole
+    run and is updated in place by SWAP primitives (a relabeling: no data
+    moves).  Uncontrolled X flips a physical tile bit (undone at the store).
+    Dense gates act on physical tile bits; diagonal factors are expressed on
+    physical bits when they are created and flushed into the next dense gate
+    on one of their bits (or into the end-of-sweep phase).
     """
-    D = geo.D
-    K = min(kmax, D)
-    low = set(range(min(low_bits, K)))
-    groups, cur, need = [], [], set()
-    for pr in prims:
-        nb = _tile_bits_needed(pr)
-        if len(need | nb | low) > K and cur:
-            groups.append((cur, need))
-            cur, need = [], set()
-        cur.append(pr)
-        need |= nb
-    if cur or not groups:
-        groups.append((cur, need))
-    out = []
-    for ops, need in groups:
-        tile = set(need) | low
-        for b in range(D):  # pad with the next lowest device bits
-            if len(tile) >= K:
-                break
-            tile.add(b)
-        out.append((ops, sorted(tile)))
-    return out
-
-
-def build_sweep(prims: list, tile: list, geo: DeviceGeometry) -> SweepProgram:
-    """Phase scheduling + virtual swaps for one sweep (physical-bit items)."""
     K = len(tile)
     tile_pos = {b: k for k, b in enumerate(tile)}
-    # reference device bit -> physical device bit / flip (tile bits only)
-    where = {b: b for b in tile}
-    flip = {b: 0 for b in tile}
+    pflip = {b: 0 for b in tile}  # physical tile bit -> value inverted
     pending: list = []  # Factor in physical device bits
     items: list = []
     const = complex(1.0)
@@ -323,8 +299,8 @@ def build_sweep(prims: list, tile: list, geo: DeviceGeometry) -> SweepProgram:
         """Reference-bit factor -> physical factors; a flipped bit reads b = 1 - p."""
         nonlocal const
         c = f.c
-        bits_p = [where.get(b, b) for b in f.bits]
-        fl = [flip.get(b, 0) for b in f.bits]
+        bits_p = [where[b] for b in f.bits]
+        fl = [pflip.get(pb, 0) for pb in bits_p]
         if not bits_p:
             const *= c
             return []
@@ -360,25 +336,25 @@ def build_sweep(prims: list, tile: list, geo: DeviceGeometry) -> SweepProgram:
                     const *= f.c
             continue
         if isinstance(pr, Swap):
-            a, b = pr.a, pr.b
-            where[a], where[b] = where[b], where[a]
-            flip[a], flip[b] = flip[b], flip[a]
+            where[pr.a], where[pr.b] = where[pr.b], where[pr.a]
             continue
         assert isinstance(pr, Dense1)
+        if pr.noop:
+            continue
         pb = where[pr.bit]
         m = pr.m
-        if flip[pr.bit]:
+        if pflip[pb]:
             m = _X @ m @ _X
         ctrl = {}
         for cb, val in pr.ctrl.items():
-            ctrl[where.get(cb, cb)] = val ^ flip.get(cb, 0)
+            pc = where[cb]
+            ctrl[pc] = val ^ pflip.get(pc, 0)
         if not ctrl and np.array_equal(m, _X):
-            flip[pr.bit] ^= 1  # virtual: relabel the bit value
+            pflip[pb] ^= 1  # virtual: relabel the bit value
             continue
         fl = flush(pb)
         if np.array_equal(m, _X):
-            # the flush must precede the data movement
-            if fl:
+            if fl:  # the flush must precede the data movement
                 items.append(_Item(OP_PH, (tile_pos[pb],), factors=fl))
             items.append(_Item(OP_X, (tile_pos[pb],), ctrl=ctrl))
             continue
@@ -394,17 +370,227 @@ def build_sweep(prims: list, tile: list, geo: DeviceGeometry) -> SweepProgram:
 
     # leftover phases are applied at the end of the sweep
     items.append(_Item(OP_PHALL, (), factors=pending))
-    out_map = {}
-    for ref, phys in where.items():
-        out_map[phys] = (ref, flip[ref])
-    sp = SweepProgram(K=K, tin=list(tile), items=items, out_map=out_map)
+    sp = SweepProgram(K=K, tin=list(tile), items=items,
+                      out_map={b: (b, pflip[b]) for b in tile})
     sp.scale = const * scale
     return sp
 
 
 # ---------------------------------------------------------------------------
-# 3. stage assignment and table generation
+# 2b. layout planner: sweep boundaries, tiles and store permutations
 # ---------------------------------------------------------------------------
+
+
+@dataclass
+class Step:
+    """One step of a device schedule, in plan order."""
+
+    kind: str  # "sweeps" (an ApplyFused task) | "exchange" | "materialize"
+    task_id: int | None = None
+    first: int = 0  # first descriptor
+    count: int = 0  # descriptors
+    swaps: list = field(default_factory=list)  # exchange: (rank int bit, physical local bit)
+
+
+@dataclass
+class DeviceProgram:
+    buf: "ProgramBuffers"
+    steps: list
+    init_perm: list  # reference device bit -> physical device bit at Alloc
+    n_fused: int
+
+
+class _Lookahead:
+    """Future needs of the remaining primitive stream, in current reference labels."""
+
+    def __init__(self, stream: list, start: int, n_local: int):
+        lab = list(range(max(n_local, 1) + 64))
+        first_use: dict = {}
+        for i in range(start, len(stream)):
+            pr = stream[i]
+            if isinstance(pr, Swap):
+                lab[pr.a], lab[pr.b] = lab[pr.b], lab[pr.a]
+            else:
+                for b in _needs(pr):
+                    cur = lab[b]
+                    if cur not in first_use:
+                        first_use[cur] = i
+        self.first_use = first_use
+        # at the end reference label y must sit at physical y; label y then is
+        # the data that now carries label lab[y]
+        self.home = {lab[y]: y for y in range(len(lab))}
+
+
+def _choose_store(tile: list, where: list, look: _Lookahead, low: int, n_local: int) -> dict:
+    """Store permutation within the tile: physical tile bit -> destination bit."""
+    inv = {p: r for r, p in enumerate(where[:n_local])}
+    ids = [inv[p] for p in tile if p in inv]  # reference labels living in the tile
+    fixed = [p for p in tile if p not in inv]  # row / phantom bits stay put
+    dest = {p: p for p in fixed}
+    free = set(p for p in tile if p in inv)
+    placed: dict = {}
+    lows = [p for p in range(low) if p in free]
+    soon = sorted((r for r in ids if r in look.first_use), key=lambda r: look.first_use[r])
+    for p, r in zip(lows, soon):
+        placed[r] = p
+    free -= set(placed.values())
+    for r in ids:
+        if r in placed:
+            continue
+        h = look.home.get(r, r)
+        if h in free:
+            placed[r] = h
+            free.discard(h)
+    for r in ids:  # the rest keep their place when possible
+        if r not in placed and where[r] in free:
+            placed[r] = where[r]
+            free.discard(where[r])
+    rest = sorted(free)
+    for r in ids:
+        if r not in placed:
+            placed[r] = rest.pop(0)
+    for r, p_new in placed.items():
+        dest[where[r]] = p_new
+    return dest
+
+
+def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_BITS,
+                max_materialize: int = 64) -> DeviceProgram:
+    """Compile every ApplyFused task of a plan for one device, with a global layout.
+
+    The physical layout is a permutation `where` of the local bits that the
+    planner owns: SWAP gates only relabel, every sweep stores its tile with a
+    permutation that parks the next sweep's qubits on the low (contiguous)
+    bits and moves other qubits toward their final position, and trailing
+    materialization sweeps restore the reference layout before the state is
+    returned.  The schedule depends only on the plan structure, so every
+    device of a distributed run derives the same layouts.
+    """
+    L, D = geo.L, geo.D
+    K = min(kmax, D)
+    low = min(low, K)
+    leaves = []
+    for task in plan.tasks:
+        if task.kind == "ApplyFused":
+            layout = plan.layout_phases[task.payload["phase"]]
+            prims = []
+            for e in task.payload["gates"]:
+                prims.extend(resolve_entry(e, layout, geo))
+            leaves.append((task.id, prims))
+    stream = [pr for _, prims in leaves for pr in prims]
+    leaf_start, pos = {}, 0
+    for tid, prims in leaves:
+        leaf_start[tid] = pos
+        pos += len(prims)
+
+    buf = ProgramBuffers()
+    steps: list = []
+    where = list(range(D))
+    # the |0...0> start is layout-invariant: pick the first layout like a store
+    look0 = _Lookahead(stream, 0, L)
+    d0 = _choose_store(list(range(L)), where, look0, low, L)
+    init = list(where)
+    for r in range(L):
+        init[r] = d0[where[r]]
+    where = list(init)
+
+    slot = 0
+    leaf_iter = iter(leaves)
+    task_leaf = {tid: prims for tid, prims in leaves}
+    for task in plan.tasks:
+        if task.kind == "Exchange":
+            sw = []
+            for s in task.payload["swaps"]:
+                ib = geo.g - 1 - s["rank_bit"]
+                sw.append((ib, where[L - 1 - s["local_bit"]]))
+            steps.append(Step("exchange", task.id, swaps=sw))
+            continue
+        if task.kind != "ApplyFused":
+            continue
+        prims = task_leaf[task.id]
+        base = leaf_start[task.id]
+        first = len(buf.descs)
+        i = 0
+        n = len(prims)
+        while True:
+            # greedy extent of this sweep under the current layout
+            trial = list(where)
+            need = set(range(low))
+            j = i
+            while j < n:
+                pr = prims[j]
+                if isinstance(pr, Swap):
+                    trial[pr.a], trial[pr.b] = trial[pr.b], trial[pr.a]
+                    j += 1
+                    continue
+                nb = {trial[b] for b in _needs(pr)}
+                if len(need | nb) > K and j > i:
+                    break
+                need |= nb
+                j += 1
+            # pad the tile with the next qubits needed after this sweep so the
+            # store can park them on the low bits
+            look = _Lookahead(stream, base + j, L)
+            tile = set(need)
+            for r in sorted(look.first_use, key=look.first_use.get):
+                if len(tile) >= K:
+                    break
+                tile.add(trial[r])
+            for b in range(D):
+                if len(tile) >= K:
+                    break
+                tile.add(b)
+            tile = sorted(tile)
+            sp = build_sweep(prims[i:j], tile, where)  # updates `where` (swaps)
+            dest = _choose_store(tile, where, look, low, L)
+            inv = {p: r for r, p in enumerate(where[:L])}
+            for p in tile:
+                _, fl = sp.out_map[p]
+                sp.out_map[p] = (dest[p], fl)
+            for p in tile:
+                if p in inv:
+                    where[inv[p]] = dest[p]
+            sp.norm_slot = slot if j >= n else -1
+            emit_sweep(sp, geo, buf)
+            i = j
+            if i >= n:
+                break
+        steps.append(Step("sweeps", task.id, first, len(buf.descs) - first))
+        slot += 1
+
+    # restore the reference layout
+    first = len(buf.descs)
+    passes = 0
+    while any(where[r] != r for r in range(L)):
+        if passes >= max_materialize:
+            raise RuntimeError("layout materialization did not converge")
+        passes += 1
+        tile = set(range(low))
+        for r in range(L):
+            if len(tile) + 2 > K:
+                break
+            if where[r] != r and (where[r] not in tile or r not in tile):
+                cand = tile | {where[r], r}
+                if len(cand) <= K:
+                    tile = cand
+        for b in range(D):
+            if len(tile) >= K:
+                break
+            tile.add(b)
+        tile = sorted(tile)
+        look = _Lookahead([], 0, L)
+        sp = build_sweep([], tile, where)
+        dest = _choose_store(tile, where, look, 0, L)
+        inv = {p: r for r, p in enumerate(where[:L])}
+        for p in tile:
+            sp.out_map[p] = (dest[p], 0)
+        for p in tile:
+            if p in inv:
+                where[inv[p]] = dest[p]
+        emit_sweep(sp, geo, buf)
+    if passes:
+        steps.append(Step("materialize", None, first, passes))
+    return DeviceProgram(buf=buf, steps=steps, init_perm=init, n_fused=slot)
 
 
 def _independent3(vs) -> bool:
@@ -684,20 +870,6 @@ def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers) -> No
         norm_slot=sp.norm_slot, cofs_index=cofs_base,
     )
     buf.descs.append(desc)
-
-
-def compile_leaf(payload: dict, layout, geo: DeviceGeometry, norm_slot: int,
-                 buf: ProgramBuffers, kmax: int = KMAX) -> int:
-    """Append the sweeps of one ApplyFused task; returns the number of sweeps."""
-    prims = []
-    for entry in payload["gates"]:
-        prims.extend(resolve_entry(entry, layout, geo))
-    groups = plan_sweeps(prims, geo, kmax)
-    for i, (ops, tile) in enumerate(groups):
-        sp = build_sweep(ops, tile, geo)
-        sp.norm_slot = norm_slot if i == len(groups) - 1 else -1
-        emit_sweep(sp, geo, buf)
-    return len(groups)
 
 
 def pack(buf: ProgramBuffers):

@@ -178,3 +178,56 @@ def _devmap(jt: np.ndarray, tin) -> np.ndarray:
     for k, b in enumerate(tin):
         out |= ((jt >> k) & 1) << b
     return out
+
+
+def emulate_plan(plan, world: int = 1, check_layout: bool = True):
+    """Run a plan through the compiled device programs of `world` devices.
+
+    Each device gets its own program (plan_device with its rank range);
+    exchanges are applied as the physical bit swaps the schedule names, on
+    the concatenation of all devices' rows.  Returns the (2^g, 2^L) blocks.
+    """
+    d, g = plan.d, plan.g
+    L = d - g
+    nr = 1 << g
+    rows = nr // world
+    h = rows.bit_length() - 1
+    progs, parts = [], []
+    for w in range(world):
+        geo = prog.DeviceGeometry(d=d, g=g, h=h, rank_base=w * rows, pad_to=prog.RB)
+        dp = prog.plan_device(plan, geo)
+        blob, descs, p = prog.pack(dp.buf)
+        progs.append((geo, dp, descs, p))
+    D = progs[0][0].D
+    # every device must derive the same layout schedule
+    if check_layout:
+        for geo, dp, _, _ in progs[1:]:
+            assert [(s.kind, s.task_id, s.swaps) for s in dp.steps] == \
+                [(s.kind, s.task_id, s.swaps) for s in progs[0][1].steps]
+    states = [np.zeros(1 << D, dtype=np.complex128) for _ in range(world)]
+    states[0][0] = 1.0
+    norms = np.zeros(max(progs[0][1].n_fused, 1))
+    steps = {s.task_id: s for s in progs[0][1].steps}
+    for task in plan.tasks:
+        st = steps.get(task.id)
+        if task.kind == "ApplyFused":
+            for w, (geo, dp, descs, p) in enumerate(progs):
+                sw = {s.task_id: s for s in dp.steps}[task.id]
+                run_sweeps(states[w], descs[sw.first: sw.first + sw.count], p, norms)
+        elif task.kind == "Exchange":
+            # global index = device * 2^(L+h) + row * 2^L + local
+            full = np.concatenate([s[: rows << L] for s in states])
+            nb = (world.bit_length() - 1) + h + L
+            x = full.reshape((2,) * nb)
+            for ib, lb in st.swaps:
+                u = L + ib
+                x = np.swapaxes(x, nb - 1 - u, nb - 1 - lb)
+            full = np.ascontiguousarray(x).reshape(-1)
+            for w in range(world):
+                states[w][: rows << L] = full[w * (rows << L):(w + 1) * (rows << L)]
+    mat = steps.get(None)
+    if mat is not None:
+        for w, (geo, dp, descs, p) in enumerate(progs):
+            run_sweeps(states[w], descs[mat.first: mat.first + mat.count], p, None)
+    blocks = np.concatenate([s[: rows << L] for s in states]).reshape(nr, 1 << L)
+    return blocks, norms

@@ -20,10 +20,7 @@ for doc in docs:
         continue
     L = plan.d - plan.g
     geo = prog.DeviceGeometry(d=plan.d, g=plan.g, h=plan.g, rank_base=0, pad_to=4)
-    buf = prog.ProgramBuffers()
-    for t in plan.tasks:
-        if t.kind == "ApplyFused":
-            prog.compile_leaf(t.payload, plan.layout_phases[t.payload["phase"]], geo, 0, buf)
+    buf = prog.plan_device(plan, geo).buf
     blob, descs, _ = prog.pack(buf)
     dblob = torch.from_numpy(blob).cuda()
     names, cubins = jit.build_kernels(buf)
