@@ -135,7 +135,7 @@ extern "C" int svb_jit_launch_sweep(void* kernel, svb_c128* state, const void* p
   if (grid > ntiles) grid = ntiles;
   const size_t smem = sizeof(double2) * ((size_t(2) << d.K) + (size_t)d.nctab);
   cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(kernel), dim3((unsigned)grid),
-                                   dim3(1u << (d.K - SVB_REG_BITS)), args, smem,
+                                   dim3(1u << (d.K - d.rb)), args, smem,
                                    as_stream(stream));
   if (e != cudaSuccess) return cuda_status(e, "jit sweep launch");
   return SVB_OK;

@@ -461,7 +461,7 @@ extern "C" int svb_run_sweeps(svb_c128* state, int64_t rows, int L, const void* 
   const char* pb = static_cast<const char*>(prog);
   for (int s = 0; s < nsweeps; ++s) {
     const svb_sweep_desc& d = desc[s];
-    if (d.K < RB || d.K > SVB_MAX_TILE_BITS_SWEEP || d.D != L + h || d.K > d.D ||
+    if (d.rb != RB || d.K < RB || d.K > SVB_MAX_TILE_BITS_SWEEP || d.D != L + h || d.K > d.D ||
         d.D > SVB_MAX_DEV_BITS) {
       set_error("sweep %d: bad geometry K=%d D=%d (L=%d, rows=%lld)", s, d.K, d.D, L,
                 (long long)rows);

@@ -94,6 +94,9 @@ def _dist_info(group=None):
 
 
 JIT_MIN_D = int(os.environ.get("SVB200_JIT_MIN_D", "16"))
+# register slots per thread in generated kernels: 3 -> 2^(K-3) = 512 threads of
+# 8 amplitudes (16 warps/SM) hides FP64 latency better than 256 x 16
+JIT_REG_BITS = int(os.environ.get("SVB200_JIT_RB", "3"))
 
 
 def _use_jit(geo: prog.DeviceGeometry, jit) -> bool:
@@ -132,7 +135,7 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None) -> _Compiled:
     if hit is not None and hit[0] is plan:
         return hit[1]
     t0 = time.perf_counter()
-    dp = prog.plan_device(plan, geo)
+    dp = prog.plan_device(plan, geo, rb=JIT_REG_BITS if use_jit else prog.RB)
     blob, descs, _ = prog.pack(dp.buf)
     host = np.ascontiguousarray(blob)
     dev_blob = torch.from_numpy(host).to(device)

@@ -32,7 +32,6 @@ CACHE_DIR = Path(os.environ.get("SVB200_JIT_CACHE", Path(__file__).resolve().par
 NVRTC_OPTS = ["--gpu-architecture=sm_100a", "--std=c++17", f"-I{CSRC}", "-lineinfo",
               "--extra-device-vectorization"]
 
-RB, NR = prog.RB, prog.NREG
 
 
 # ---------------------------------------------------------------------------
@@ -102,7 +101,9 @@ def _xor_img(var: str, imgs) -> str:
 
 def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
     K, D = desc["K"], desc["D"]
-    NT = 1 << (K - RB)
+    rb = int(desc.get("rb", prog.RB)) if hasattr(desc, "get") else int(desc["rb"])
+    NR = 1 << rb
+    NT = 1 << (K - rb)
     tin = list(desc["tin"])[:K]
     sw = list(desc["sw"])[:K]
     st_dev = list(desc["st_dev"])[:K]
@@ -111,7 +112,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
     nct = int(desc["nctab"])
     fbits = [b for b in range(D) if b not in tin]
     ntiles = 1 << (D - K)
-    tb = K - RB  # thread bits
+    tb = K - rb  # thread bits
 
     L = []
     w = L.append
@@ -128,6 +129,9 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
     w(f"  const u32 lds_t = {_xor_img('t', sw[:tb])};")
     w(f"  const u64 st_t = {_deposit('t', st_dev[:tb])};")
     w(f"  const u32 sts_t = {_xor_img('t', st_sw[:tb])};")
+    # per-thread phase tables do not depend on the tile: load them once
+    for off in sorted({int(op["tab"]) for op in ops if op["kind"] != prog.OP_STAGE and int(op["tab"]) >= 0}):
+        w(f"  const double2 tab{off} = __ldg(tab + {off} + t);")
     stages = [op for op in ops if op["kind"] == prog.OP_STAGE]
     stage_info = []
     for si, st in enumerate(stages):
@@ -139,7 +143,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
         offs = []
         for v in range(NR):
             o = 0
-            for q in range(RB):
+            for q in range(rb):
                 if (v >> q) & 1:
                     o ^= sw[regs[q]]
             offs.append(o)
@@ -155,7 +159,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
         for it in range(NR):
             dev = 0
             s = 0
-            for q in range(RB):
+            for q in range(rb):
                 if (it >> q) & 1:
                     dev |= 1 << tin[tb + q]
                     s ^= sw[tb + q]
@@ -180,7 +184,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
     w(f"      double2* const nbuf = (iter & 1) ? smem : smem + {1 << K};")
     prefetch("nbuf", "bn")
     w("    }")
-    w("    double2 x[16];")
+    w(f"    double2 x[{NR}];")
 
     cur = None  # current stage index
     for op in ops:
@@ -197,7 +201,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
                 w(f"    x[{v}] = tile[sb{nxt} ^ {offs[v]}u];")
             cur = nxt
             continue
-        _emit_op(w, op, coef, cur, K)
+        _emit_op(w, op, coef, cur, K, rb)
 
     if cur is not None:
         _, _, offs = stage_info[cur]
@@ -207,7 +211,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
     for it in range(NR):
         dev = 0
         s = 0
-        for q in range(RB):
+        for q in range(rb):
             if (it >> q) & 1:
                 dev |= 1 << st_dev[tb + q]
                 s ^= st_sw[tb + q]
@@ -235,19 +239,20 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
     return "\n".join(L) + "\n"
 
 
-def _phase_base(w, op, coef_c0: complex, K: int) -> None:
+def _phase_base(w, op, coef_c0: complex, K: int, rb: int) -> None:
     """Emit `p` = const * per-tile slot * per-thread table * per-thread-bit slots."""
     w(f"      double2 p = make_double2({_lit(coef_c0.real)}, {_lit(coef_c0.imag)});")
     if int(op["ctab"]) >= 0:
         w(f"      p = cmul(p, ctab[{int(op['ctab'])}]);")
     if int(op["tab"]) >= 0:
-        w(f"      p = cmul(p, __ldg(tab + {int(op['tab'])} + t));")
+        w(f"      p = cmul(p, tab{int(op['tab'])});")
     if int(op["tf"]) >= 0:
-        for i in range(K - RB):
+        for i in range(K - rb):
             w(f"      if ((t >> {i}) & 1) p = cmul(p, ctab[{int(op['tf']) + i}]);")
 
 
-def _emit_op(w, op, coef, stage, K) -> None:
+def _emit_op(w, op, coef, stage, K, rb) -> None:
+    NR = 1 << rb
     kind = int(op["kind"])
     a = int(op["a"])
     A = 1 << a
@@ -262,10 +267,10 @@ def _emit_op(w, op, coef, stage, K) -> None:
         fused = False
         if has_phase:
             ph = cf if kind == prog.OP_PH else cf + 4
-            _phase_base(w, op, coef[ph], K)
+            _phase_base(w, op, coef[ph], K, rb)
             nt = (int(op["flags"]) >> prog.F_PREG_SHIFT) & 0xF
             fused = kind == prog.OP_H and cm == 0
-            _emit_dfs(w, a, nt, [coef[ph + 1 + s] for s in range(RB)], fused)
+            _emit_dfs(w, a, nt, [coef[ph + 1 + s] for s in range(rb)], fused, rb)
         if kind == prog.OP_H and not fused:
             for v in range(NR):
                 if (v & A) or (v & cm) != cv:
@@ -299,7 +304,7 @@ def _emit_op(w, op, coef, stage, K) -> None:
                 w(f"        x[{idx[r]}] = {_lincomb([(M[r, c], f'a{c}') for c in range(4)])};")
             w("      }")
     elif kind == prog.OP_PHALL:
-        _phase_base(w, op, coef[cf], K)
+        _phase_base(w, op, coef[cf], K, rb)
         for v in range(NR):
             w(f"      x[{v}] = cmul(x[{v}], p);")
     elif kind == prog.OP_SCALE:
@@ -310,12 +315,12 @@ def _emit_op(w, op, coef, stage, K) -> None:
     w("    }")
 
 
-def _emit_dfs(w, a: int, nt: int, c: list, fused_h: bool) -> None:
+def _emit_dfs(w, a: int, nt: int, c: list, fused_h: bool, rb: int) -> None:
     """Depth-first product over register slots != a; leaves are amplitudes with bit a set."""
     counter = [0]
 
     def rec(s, v, pv):
-        if s == RB:
+        if s == rb:
             if fused_h:
                 w(f"      {{ const double2 x1 = cmul(x[{v}], {pv}); const double2 x0 = x[{v ^ (1 << a)}]; "
                   f"x[{v ^ (1 << a)}] = cadd(x0, x1); x[{v}] = csub(x0, x1); }}")
@@ -378,6 +383,7 @@ def _compile(src: str, name: str) -> bytes:
 
 
 def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: int | None = None):
+    """One kernel per descriptor; register-slot count per sweep comes from the descriptor."""
     """Generate + compile one kernel per sweep descriptor; returns (names, cubins, hashes)."""
     srcs, names = [], []
     for i, d in enumerate(buf.descs):

@@ -66,6 +66,7 @@ DESC_DTYPE = np.dtype(
         ("st_flip", "<u8"),
         ("op_begin", "<i4"), ("op_count", "<i4"),
         ("nctab", "<i4"), ("norm_slot", "<i4"),
+        ("rb", "<i4"), ("pad0", "<i4"),
         ("ops_off", "<i8"), ("coef_off", "<i8"), ("tab_off", "<i8"),
         ("cterm_off", "<i8"), ("cofs_off", "<i8"),
     ],
@@ -455,7 +456,7 @@ def _choose_store(tile: list, where: list, look: _Lookahead, low: int, n_local: 
 
 
 def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_BITS,
-                max_materialize: int = 64) -> DeviceProgram:
+                max_materialize: int = 64, rb: int = RB) -> DeviceProgram:
     """Compile every ApplyFused task of a plan for one device, with a global layout.
 
     The physical layout is a permutation `where` of the local bits that the
@@ -551,7 +552,7 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
                 if p in inv:
                     where[inv[p]] = dest[p]
             sp.norm_slot = slot if j >= n else -1
-            emit_sweep(sp, geo, buf)
+            emit_sweep(sp, geo, buf, rb)
             i = j
             if i >= n:
                 break
@@ -587,7 +588,7 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
         for p in tile:
             if p in inv:
                 where[inv[p]] = dest[p]
-        emit_sweep(sp, geo, buf)
+        emit_sweep(sp, geo, buf, rb)
     if passes:
         steps.append(Step("materialize", None, first, passes))
     return DeviceProgram(buf=buf, steps=steps, init_perm=init, n_fused=slot)
@@ -627,13 +628,13 @@ def _choose_swizzle(K: int, patterns: list, seed: int = 0) -> list:
     return [(1 << k) if k < 3 else ((1 << k) | lows[k]) for k in range(K)]
 
 
-def _stages(items: list) -> list:
-    """Group items into stages of <= 4 register bits; returns [(rbits, items)]."""
+def _stages(items: list, rb: int = RB) -> list:
+    """Group items into stages of <= rb register bits; returns [(rbits, items)]."""
     stages = []
     cur, need = [], set()
     for it in items:
         nb = set(it.bits)
-        if len(need | nb) > RB and cur:
+        if len(need | nb) > rb and cur:
             stages.append([need, cur])
             cur, need = [], set()
         cur.append(it)
@@ -665,29 +666,29 @@ class ProgramBuffers:
         return off
 
 
-def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers) -> None:
+def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers, rb: int = RB) -> None:
     K = sp.K
     tin = sp.tin
     dev_to_tile = {b: k for k, b in enumerate(tin)}
-    NT = 1 << (K - RB)
+    NT = 1 << (K - rb)
     tidx = np.arange(NT, dtype=np.int64)
 
     items = list(sp.items)
     # fold the accumulated constant / H scale into the final phase item
     final = items[-1]
     assert final.kind == OP_PHALL
-    stages = _stages([it for it in items if it.kind != OP_PHALL])
+    stages = _stages([it for it in items if it.kind != OP_PHALL], rb)
     if not stages and (final.factors or sp.scale != 1):
         stages = [[set(), []]]
-    # pad register sets to exactly RB bits, preferring bits used soon after
+    # pad register sets to exactly rb bits, preferring bits used soon after
     for si, st in enumerate(stages):
         need = st[0]
         for later in stages[si + 1:]:
             for b in sorted(later[0]):
-                if len(need) < RB and b not in need:
+                if len(need) < rb and b not in need:
                     need.add(b)
         for b in range(K):
-            if len(need) >= RB:
+            if len(need) >= rb:
                 break
             need.add(b)
         st[0] = need
@@ -711,8 +712,8 @@ def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers) -> No
     # smem swizzle: load (tile bits 0..2), store order, each stage's thread bits
     store_order = sorted(range(K), key=lambda k: sp.out_map[tin[k]][0])
     patterns = [[0, 1, 2], store_order[:3]]
-    for rb, _ in stages:
-        comp = [k for k in range(K) if k not in rb]
+    for rbits_s, _ in stages:
+        comp = [k for k in range(K) if k not in rbits_s]
         patterns.append(comp[:3])
     sw = _choose_swizzle(K, [p for p in patterns if len(p) == 3])
 
@@ -751,7 +752,7 @@ def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers) -> No
                     op["pval"] |= val << cb
             # phase factors -> (const, per-thread table, per-tile slots, register factors)
             pre_const = complex(1.0)
-            preg = [complex(1.0)] * RB
+            preg = [complex(1.0)] * rb
             tab = None
             tf_terms: dict = {}
             scal_terms: list = []
@@ -808,7 +809,7 @@ def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers) -> No
                     op["ctab"] = s
                 if tf_terms:
                     first = None
-                    for i in range(K - RB):
+                    for i in range(K - rb):
                         s = new_ctab()
                         if first is None:
                             first = s
@@ -817,7 +818,7 @@ def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers) -> No
                 if tab is not None:
                     op["tab"] = buf.add_tab(tab)
                 nt = 0
-                for i in range(RB):
+                for i in range(rb):
                     if preg[i] != 1:
                         nt |= 1 << i
                 op["flags"] |= nt << F_PREG_SHIFT
@@ -867,7 +868,7 @@ def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers) -> No
         K=K, D=geo.D, tin=list(tin), sw=sw,
         st_dev=[tout[k] for k in store_order], st_sw=[sw[k] for k in store_order],
         st_flip=st_flip, op_begin=op_begin, op_count=op_count, nctab=nct[0],
-        norm_slot=sp.norm_slot, cofs_index=cofs_base,
+        norm_slot=sp.norm_slot, cofs_index=cofs_base, rb=rb,
     )
     buf.descs.append(desc)
 
@@ -921,6 +922,7 @@ def pack(buf: ProgramBuffers):
         e["st_flip"] = d["st_flip"]
         e["op_begin"], e["op_count"] = d["op_begin"], d["op_count"]
         e["nctab"], e["norm_slot"] = d["nctab"], d["norm_slot"]
+        e["rb"] = d.get("rb", RB)
         e["ops_off"], e["coef_off"], e["tab_off"] = ops_off, coef_off, tab_off
         e["cterm_off"] = ct_off
         e["cofs_off"] = cofs_off + 4 * d["cofs_index"]

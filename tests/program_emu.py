@@ -14,7 +14,6 @@ import numpy as np
 
 from paper_2509_14098_b200 import program as prog
 
-RB, NR = prog.RB, prog.NREG
 
 
 def _dep(vals: np.ndarray, bits) -> np.ndarray:
@@ -37,6 +36,8 @@ def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None)
     cofs_base = 0
     for d in descs:
         K, D = int(d["K"]), int(d["D"])
+        RB = int(d["rb"])
+        NR = 1 << RB
         NT = 1 << (K - RB)
         tin = [int(x) for x in d["tin"][:K]]
         sw = [int(x) for x in d["sw"][:K]]
@@ -180,7 +181,7 @@ def _devmap(jt: np.ndarray, tin) -> np.ndarray:
     return out
 
 
-def emulate_plan(plan, world: int = 1, check_layout: bool = True):
+def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog.RB):
     """Run a plan through the compiled device programs of `world` devices.
 
     Each device gets its own program (plan_device with its rank range);
@@ -195,7 +196,7 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True):
     progs, parts = [], []
     for w in range(world):
         geo = prog.DeviceGeometry(d=d, g=g, h=h, rank_base=w * rows, pad_to=prog.RB)
-        dp = prog.plan_device(plan, geo)
+        dp = prog.plan_device(plan, geo, rb=rb)
         blob, descs, p = prog.pack(dp.buf)
         progs.append((geo, dp, descs, p))
     D = progs[0][0].D

@@ -17,11 +17,12 @@ def _cases(grid_docs, grid_states, limit=None, min_ranks=1):
     return out[:limit] if limit else out
 
 
-def test_single_device_programs_match_reference(grid_docs, grid_states):
+@pytest.mark.parametrize("rb", [4, 3])
+def test_single_device_programs_match_reference(grid_docs, grid_states, rb):
     worst = 0.0
     for doc in _cases(grid_docs, grid_states):
         plan = plan_from_doc(doc["plan"])
-        blocks, norms = program_emu.emulate_plan(plan)
+        blocks, norms = program_emu.emulate_plan(plan, rb=rb)
         err = float(np.max(np.abs(blocks - grid_states[doc["name"]])))
         assert err < TOL, (doc["name"], err)
         assert np.all(np.abs(norms - 1) < 1e-8), doc["name"]
