@@ -277,7 +277,13 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             if state is None:
                 fail(PlanInvalid("compute before Alloc"))
             st = compiled.steps[task.id]
-            _run_descs(compiled, st.first, st.count, state, rows_eff, L, norms, grid_limit, stream)
+            slot = len(fused_order)
+            if st.count:
+                _run_descs(compiled, st.first, st.count, state, rows_eff, L, norms, grid_limit, stream)
+            elif slot > 0:  # relabel-only leaf: the state (and its norm) is unchanged
+                norms[slot:slot + 1].copy_(norms[slot - 1:slot])
+            else:
+                lib.svb_norm2(state.buf.data_ptr(), rows << L, norms[slot:].data_ptr(), stream)
             count = st.count
             stats.sweeps += count
             stats.kernel_launches += count

@@ -455,6 +455,19 @@ def _choose_store(tile: list, where: list, look: _Lookahead, low: int, n_local: 
     return dest
 
 
+def _pad_displaced(tile: set, where: list, look: _Lookahead, K: int, L: int) -> None:
+    """Fill free tile slots with (position, home) pairs of displaced qubits."""
+    for r in range(L):
+        if len(tile) >= K:
+            return
+        h = look.home.get(r, r)
+        if h >= L or where[r] == h:
+            continue
+        add = {where[r], h} - tile
+        if len(tile) + len(add) <= K:
+            tile |= add
+
+
 def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_BITS,
                 max_materialize: int = 64, rb: int = RB) -> DeviceProgram:
     """Compile every ApplyFused task of a plan for one device, with a global layout.
@@ -513,6 +526,13 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
         first = len(buf.descs)
         i = 0
         n = len(prims)
+        if all(isinstance(pr, Swap) for pr in prims):
+            # a pure relabeling: no data moves, the norm is unchanged
+            for pr in prims:
+                where[pr.a], where[pr.b] = where[pr.b], where[pr.a]
+            steps.append(Step("sweeps", task.id, first, 0))
+            slot += 1
+            continue
         while True:
             # greedy extent of this sweep under the current layout
             trial = list(where)
@@ -537,6 +557,7 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
                 if len(tile) >= K:
                     break
                 tile.add(trial[r])
+            _pad_displaced(tile, trial, look, K, L)
             for b in range(D):
                 if len(tile) >= K:
                     break

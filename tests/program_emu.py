@@ -212,9 +212,12 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
     for task in plan.tasks:
         st = steps.get(task.id)
         if task.kind == "ApplyFused":
+            slot = sum(1 for t in plan.tasks[: plan.tasks.index(task)] if t.kind == "ApplyFused")
             for w, (geo, dp, descs, p) in enumerate(progs):
                 sw = {s.task_id: s for s in dp.steps}[task.id]
                 run_sweeps(states[w], descs[sw.first: sw.first + sw.count], p, norms)
+            if st.count == 0:
+                norms[slot] = norms[slot - 1] if slot else sum(float(np.sum(np.abs(s) ** 2)) for s in states)
         elif task.kind == "Exchange":
             # global index = device * 2^(L+h) + row * 2^L + local
             full = np.concatenate([s[: rows << L] for s in states])
