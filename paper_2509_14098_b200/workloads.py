@@ -172,3 +172,41 @@ FAMILIES = {
     "qaoa": qaoa_maxcut,
     "supremacy": random_supremacy,
 }
+
+
+_SELF_INVERSE = {"id", "h", "x", "y", "z", "cx", "cz", "swap", "ccx"}
+_SWAP_INV = {"t": "tdg", "tdg": "t", "s": "sdg", "sdg": "s"}
+_NEG = {"rx", "ry", "rz", "p", "cp"}
+
+
+def _inverse_line(line: str) -> str:
+    """Inverse of one gate statement of the reference gate set."""
+    stmt = line.strip().rstrip(";")
+    head, _, args = stmt.partition(" ")
+    name, _, par = head.partition("(")
+    par = par.rstrip(")")
+    if name in _SELF_INVERSE:
+        return line
+    if name in _SWAP_INV:
+        return f"{_SWAP_INV[name]} {args};"
+    if name in _NEG:
+        return f"{name}(-({par})) {args};"
+    if name == "u":  # u(t, f, l)^dagger = u(-t, -l, -f)
+        t, f, lam = (x.strip() for x in par.split(","))
+        return f"u(-({t}),-({lam}),-({f})) {args};"
+    raise ValueError(f"no inverse for {name}")
+
+
+def mirror(qasm: str) -> str:
+    """U followed by U^dagger: the exact output is |0...0> (a full-size known answer)."""
+    lines = qasm.strip().splitlines()
+    head = [ln for ln in lines if ln.startswith(("OPENQASM", "include", "qreg"))]
+    body = [ln for ln in lines if ln not in head and ln.strip()]
+    return "\n".join(head + body + [_inverse_line(ln) for ln in reversed(body)]) + "\n"
+
+
+def basis_qft_amplitudes(d: int, x: int, y):
+    """Closed form of the reference QFT (svpart/circuits.py:34-42) on |x>:
+    amp(y) = 2^(-d/2) exp(-2 pi i x y / 2^d), qubit 0 the most significant bit."""
+    xy = (np.asarray(y, dtype=np.int64) * x) & ((1 << d) - 1)
+    return np.exp(-2j * np.pi * xy / (1 << d)) / (2 ** (d / 2))

@@ -203,6 +203,11 @@ BENCH = [
     ("qft22_h22-12", lambda: workloads.qft(22), [22, 12]),
     ("qft23_h23-12", lambda: workloads.qft(23), [23, 12]),
     ("qv22_h22-12", lambda: workloads.quantum_volume(22, seed=22), [22, 12]),
+    ("qft28_h28-12", lambda: workloads.qft(28), [28, 12]),
+    ("mirror_qv24_h22-12", lambda: workloads.mirror(workloads.quantum_volume(24, seed=5)), [22, 12]),
+    ("mirror_qaoa24_h24-12", lambda: workloads.mirror(workloads.qaoa_maxcut(24, seed=6)), [24, 12]),
+    ("mirror_sup24_h21-12", lambda: workloads.mirror(workloads.random_supremacy(24, seed=7)), [21, 12]),
+    ("mirror_qv28_h28-12", lambda: workloads.mirror(workloads.quantum_volume(28, seed=8, depth=12)), [28, 12]),
 ]
 
 

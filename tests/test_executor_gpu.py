@@ -1,0 +1,159 @@
+"""Executor API semantics on the GPU, mirroring the reference's test_executor.py cases."""
+
+import numpy as np
+import pytest
+
+from conftest import plan_from_doc
+
+pytestmark = pytest.mark.gpu
+
+
+def _plan(grid_docs, name):
+    return plan_from_doc(next(d for d in grid_docs if d["name"] == name)["plan"])
+
+
+def test_ghz3_final_state_and_stats(grid_docs):
+    # test_executor.py:29-47
+    from paper_2509_14098_b200 import gather, run_plan
+
+    res = run_plan(_plan(grid_docs, "ghz3-2"))
+    dense = gather(res.state)
+    exp = np.zeros(8, dtype=complex)
+    exp[0] = exp[7] = 2 ** -0.5
+    np.testing.assert_allclose(dense, exp, atol=1e-12)
+    assert res.stats.task_counts == {"Alloc": 1, "ApplyFused": 2, "Pack": 1, "Exchange": 1,
+                                     "Unpack": 1, "Free": 1}
+    (e,) = res.stats.exchanges
+    assert e["messages"] == 2 and e["amps"] // e["messages"] == 2 and e["bytes"] == 16 * e["amps"]
+
+
+def test_initial_state_and_drift(grid_docs):
+    # test_executor.py:104-117
+    from paper_2509_14098_b200 import NonUnitaryDrift, gather, run_plan
+
+    plan = _plan(grid_docs, "x0-2")
+    init = np.zeros(4, dtype=complex)
+    init[1] = 1.0
+    dense = gather(run_plan(plan, initial=init).state)
+    np.testing.assert_allclose(dense, np.eye(4)[3], atol=1e-12)
+    with pytest.raises(NonUnitaryDrift):
+        run_plan(plan, initial=np.full(4, 0.9, dtype=complex))
+
+
+def test_protocol_errors(grid_docs):
+    # test_executor.py:146-175
+    from paper_2509_14098_b200 import PlanInvalid, run_plan
+    from paper_2509_14098_b200.plan import ExecutionPlan, Task
+
+    plan = _plan(grid_docs, "ghz3-2")
+    t = list(plan.tasks)
+    t[1], t[5] = t[5], t[1]
+    with pytest.raises(PlanInvalid):
+        run_plan(ExecutionPlan(plan.d, plan.g, plan.layout_phases, t))
+    extra = Task(len(plan.tasks), "Alloc", (len(plan.tasks) - 1,), plan.tasks[0].payload)
+    with pytest.raises(PlanInvalid):
+        run_plan(ExecutionPlan(plan.d, plan.g, plan.layout_phases, list(plan.tasks) + [extra]))
+    nopack = [x for x in plan.tasks if x.kind != "Pack"]
+    nopack = [Task(i, x.kind, (i - 1,) if i else (), x.payload) for i, x in enumerate(nopack)]
+    with pytest.raises(PlanInvalid):
+        run_plan(ExecutionPlan(plan.d, plan.g, plan.layout_phases, nopack))
+    # stale passthrough mark
+    bad = [Task(x.id, x.kind, x.deps, dict(x.payload)) for x in plan.tasks]
+    g0 = dict(bad[1].payload["gates"][0])
+    g0["passthrough"] = not g0["passthrough"]
+    bad[1].payload["gates"] = [g0] + bad[1].payload["gates"][1:]
+    with pytest.raises(PlanInvalid):
+        run_plan(ExecutionPlan(plan.d, plan.g, plan.layout_phases, bad))
+
+
+def test_scatter_gather_compare(grid_docs):
+    # test_executor.py:66-101
+    from paper_2509_14098_b200 import DimensionMismatch, compare, gather, scatter
+
+    plan = _plan(grid_docs, "ghz3-2")
+    rng = np.random.default_rng(5)
+    v = rng.normal(size=8) + 1j * rng.normal(size=8)
+    v /= np.linalg.norm(v)
+    for ph in (0, 1):
+        np.testing.assert_allclose(gather(scatter(v, plan, ph)), v, atol=1e-15)
+    w = np.exp(1j * 1.234) * v
+    assert compare(v, w) < 1e-12 and compare(v, v) == 0.0
+    a = np.zeros(4, dtype=complex)
+    a[0] = 1
+    b = np.zeros(4, dtype=complex)
+    b[1] = 1
+    assert compare(a, b) > 0.9
+    with pytest.raises(DimensionMismatch):
+        scatter(np.zeros(4, dtype=complex), plan)
+    with pytest.raises(DimensionMismatch):
+        compare(a, np.zeros(8, dtype=complex))
+
+
+def test_histograms(grid_docs):
+    # test_executor.py:128-143 + bit-identity with the reference sampler
+    from paper_2509_14098_b200 import run_plan, sample
+
+    plan = _plan(grid_docs, "ghz3-2")
+    r1 = run_plan(plan, shots=200, seed=9)
+    r2 = run_plan(plan, shots=200, seed=9)
+    assert r1.histogram == r2.histogram and sum(r1.histogram.values()) == 200
+    assert set(r1.histogram) <= {"000", "111"}
+    d = np.zeros(4, dtype=complex)
+    d[2] = 1
+    assert sample(d, 50, seed=1) == {"10": 50}
+
+
+def test_oracle_simulate_and_size_guard(grid_docs, grid_states):
+    from paper_2509_14098_b200 import TooLarge, compare, oracle_simulate
+
+    class Op:
+        def __init__(self, kind, params, qubits):
+            from paper_2509_14098_b200 import gates
+            self.gate = gates.gate(kind, tuple(params))
+            self.qubits = tuple(qubits)
+
+    class Circ:
+        def __init__(self, d, ops):
+            self.num_qubits, self.ops = d, ops
+
+    n = 0
+    for doc in grid_docs:
+        if doc["name"] + "::dense" not in grid_states or doc["plan"]["d"] > 10 or n > 40:
+            continue
+        ops = [Op(g["kind"], g["params"], g["qubits"]) for t in doc["plan"]["tasks"]
+               if t["kind"] == "ApplyFused" for g in t["payload"]["gates"]]
+        v = oracle_simulate(Circ(doc["plan"]["d"], ops))
+        assert compare(v, grid_states[doc["name"] + "::dense"]) < 1e-10, doc["name"]
+        n += 1
+    with pytest.raises(TooLarge):
+        oracle_simulate(Circ(15, []))
+
+
+def test_kernel_plugin_matches_numpy():
+    # test_kernels.py:33-81: GPU plugin vs the numpy twin, random unitaries/diagonals
+    from oracle.oracle import _NumpyKernels
+    from paper_2509_14098_b200 import kernels
+
+    rng = np.random.default_rng(3)
+    for _ in range(40):
+        L = int(rng.integers(1, 9))
+        ranks = 1 << int(rng.integers(0, 3))
+        p = int(rng.integers(1, min(L, 4) + 1))
+        bits = [int(b) for b in rng.permutation(L)[:p]]
+        m = rng.normal(size=(1 << p, 1 << p)) + 1j * rng.normal(size=(1 << p, 1 << p))
+        u, _ = np.linalg.qr(m)
+        a = rng.normal(size=(ranks, 1 << L)) + 1j * rng.normal(size=(ranks, 1 << L))
+        b = a.copy()
+        _NumpyKernels.apply_gate(a, u, bits)
+        kernels.apply_gate(b, u, bits)
+        np.testing.assert_allclose(a, b, atol=1e-12)
+        dg = np.exp(1j * rng.uniform(-3, 3, size=1 << p))
+        _NumpyKernels.apply_diagonal(a, dg, bits)
+        kernels.apply_diagonal(b, dg, bits)
+        np.testing.assert_allclose(a, b, atol=1e-12)
+    with pytest.raises(ValueError):
+        kernels.core_apply_gate(np.zeros((1, 4), complex), np.eye(4, dtype=complex), [0])
+    big = np.zeros((1, 1 << 8), complex)
+    big[0, 0] = 1
+    kernels.apply_gate(big, np.linalg.qr(rng.normal(size=(128, 128)))[0].astype(complex), list(range(7)))
+    assert abs(np.linalg.norm(big) - 1) < 1e-10
