@@ -38,7 +38,7 @@ __global__ void k_argmax_w(const double2* __restrict__ a, const double2* __restr
   WI best{-1.0, INT64_MAX};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    best = better(best, WI{cabs_(a[i]) * cabs_(b[i]), i});
+    best = better(best, WI{__dmul_rn(cabs_(a[i]), cabs_(b[i])), i});
   }
   sh[threadIdx.x] = best;
   __syncthreads();
@@ -66,8 +66,9 @@ __global__ void k_maxdev(const double2* __restrict__ a, const double2* __restric
     double2 phi = make_double2(1.0, 0.0);
     if (sh[0].w > 0.0) {
       const double2 ak = a[sh[0].i], bk = b[sh[0].i];
-      // z = a_k * conj(b_k); phi = z / |z|
-      const double2 z = make_double2(ak.x * bk.x + ak.y * bk.y, ak.y * bk.x - ak.x * bk.y);
+      // z = a_k * conj(b_k); phi = z / |z|, with numpy's (uncontracted) rounding
+      const double2 z = make_double2(__dadd_rn(__dmul_rn(ak.x, bk.x), __dmul_rn(ak.y, bk.y)),
+                                     __dsub_rn(__dmul_rn(ak.y, bk.x), __dmul_rn(ak.x, bk.y)));
       const double az = cabs_(z);
       phi = make_double2(z.x / az, z.y / az);
     }
@@ -79,8 +80,9 @@ __global__ void k_maxdev(const double2* __restrict__ a, const double2* __restric
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double2 bi = b[i], ai = a[i];
-    const double2 pb = make_double2(phi.x * bi.x - phi.y * bi.y, phi.x * bi.y + phi.y * bi.x);
-    m = fmax(m, cabs_(make_double2(ai.x - pb.x, ai.y - pb.y)));
+    const double2 pb = make_double2(__dsub_rn(__dmul_rn(phi.x, bi.x), __dmul_rn(phi.y, bi.y)),
+                                    __dadd_rn(__dmul_rn(phi.x, bi.y), __dmul_rn(phi.y, bi.x)));
+    m = fmax(m, cabs_(make_double2(__dsub_rn(ai.x, pb.x), __dsub_rn(ai.y, pb.y))));
   }
   __shared__ double shm[kThreads];
   shm[threadIdx.x] = m;

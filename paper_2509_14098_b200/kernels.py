@@ -41,7 +41,7 @@ def _call(fn_name: str, blocks, table, bits, width: int):
     dev, host = _device_blocks(blocks)
     if dev.dim() != 2:
         raise ValueError("blocks must be 2-D (ranks, 2^L)")
-    t = torch.from_numpy(np.ascontiguousarray(table, dtype=np.complex128).reshape(-1)).to(dev.device)
+    t = torch.from_numpy(np.array(table, dtype=np.complex128, copy=True).reshape(-1)).to(dev.device)
     arr, ptr = _native.i64_array(list(bits))
     dim = int(np.asarray(table).shape[0])
     rc = getattr(lib, fn_name)(dev.data_ptr(), dev.shape[0], dev.shape[1], t.data_ptr(), dim,
