@@ -98,23 +98,41 @@ def exchange(state, remote: list, geo, group, mover=None, chunk_elems: int | Non
         chunk_elems = max(1, min(region, CHUNK_BYTES // 16))
     mover = mover or CudaMover(state)
     dev = state.buf.device
+    L = state.L
+    # contiguous fast path: the swapped local bits are the top physical bits,
+    # so every region is one contiguous block that NCCL can send in place
+    contiguous = state.rows == 1 and sorted(lbits) == list(range(L - m, L))
     nbuf = 2
-    send = [torch.empty((len(peers), chunk_elems), dtype=torch.complex128, device=dev) for _ in range(nbuf)]
+    send = [torch.empty((len(peers), chunk_elems), dtype=torch.complex128, device=dev)
+            for _ in range(nbuf)] if not contiguous else None
     recv = [torch.empty((len(peers), chunk_elems), dtype=torch.complex128, device=dev) for _ in range(nbuf)]
     launches = 0
     nchunks = (region + chunk_elems - 1) // chunk_elems
+
+    def region_base(sel):
+        base = 0
+        for i, lb in enumerate(lbits):
+            if (sel >> (m - 1 - i)) & 1:
+                base |= 1 << lb
+        return base
 
     def issue(c):
         nonlocal launches
         off = c * chunk_elems
         cnt = min(chunk_elems, region - off)
         b = c % nbuf
+        srcs = []
         for j, pp in enumerate(peers):
-            mover.pack(lbits, m, pp.sel, off, cnt, send[b][j])
-            launches += 1
+            if contiguous:
+                a0 = region_base(pp.sel) + off
+                srcs.append(state.buf[a0:a0 + cnt])
+            else:
+                mover.pack(lbits, m, pp.sel, off, cnt, send[b][j])
+                launches += 1
+                srcs.append(send[b][j, :cnt])
         ops = []
         for j, pp in enumerate(peers):
-            ops.append(dist.P2POp(dist.isend, _as_real(send[b][j, :cnt]), pp.peer, group))
+            ops.append(dist.P2POp(dist.isend, _as_real(srcs[j]), pp.peer, group))
             ops.append(dist.P2POp(dist.irecv, _as_real(recv[b][j, :cnt]), pp.peer, group))
         return dist.batch_isend_irecv(ops), off, cnt, b
 
@@ -125,7 +143,11 @@ def exchange(state, remote: list, geo, group, mover=None, chunk_elems: int | Non
         for w in works:
             w.wait()
         for j, pp in enumerate(peers):
-            mover.unpack(lbits, m, pp.sel, off, cnt, recv[b][j])
-            launches += 1
+            if contiguous:
+                a0 = region_base(pp.sel) + off
+                state.buf[a0:a0 + cnt].copy_(recv[b][j, :cnt])
+            else:
+                mover.unpack(lbits, m, pp.sel, off, cnt, recv[b][j])
+                launches += 1
         pending = nxt
     return launches

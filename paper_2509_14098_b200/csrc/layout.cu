@@ -50,33 +50,35 @@ __global__ void k_bitswap(double2* __restrict__ s, BitSwap bs, uint64_t total) {
 struct Region {
   int L, m;
   uint64_t selmask;  // sel deposited into lbits
-  int free_bits[64];
-  int nfree;  // L - m local bits not in lbits, ascending
+  int nchunks;       // 8-bit chunks of the element index
+  uint64_t lut[5 * 256];  // deposit of element-index chunks into the free bits
 };
 
-__device__ __forceinline__ uint64_t region_index(const Region& r, uint64_t k) {
+__device__ __forceinline__ uint64_t region_index(const uint64_t* lut, int nchunks, int L, int m,
+                                                 uint64_t selmask, uint64_t k) {
   // k = row * 2^(L-m) + e  ->  row * 2^L + deposit(e) | selmask
-  const int eb = r.L - r.m;
+  const int eb = L - m;
   const uint64_t row = k >> eb;
-  uint64_t e = k & ((uint64_t(1) << eb) - 1);
-  uint64_t loc = r.selmask;
-  for (int i = 0; i < r.nfree && e; ++i, e >>= 1)
-    if (e & 1) loc |= uint64_t(1) << r.free_bits[i];
-  return (row << r.L) | loc;
+  const uint64_t e = k & ((uint64_t(1) << eb) - 1);
+  uint64_t loc = selmask;
+  for (int c = 0; c < nchunks; ++c) loc |= lut[c * 256 + ((e >> (8 * c)) & 255)];
+  return (row << L) | loc;
 }
 
-__global__ void k_pack(const double2* __restrict__ s, Region r, int64_t off, int64_t count,
-                       double2* __restrict__ out) {
+template <bool PACK>
+__global__ void k_region(double2* __restrict__ s, const __grid_constant__ Region r, int64_t off,
+                         int64_t count, double2* __restrict__ buf) {
+  __shared__ uint64_t lut[5 * 256];
+  for (int i = threadIdx.x; i < r.nchunks * 256; i += blockDim.x) lut[i] = r.lut[i];
+  __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = s[region_index(r, (uint64_t)(off + i))];
-}
-
-__global__ void k_unpack(double2* __restrict__ s, Region r, int64_t off, int64_t count,
-                         const double2* __restrict__ in) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-       i += (int64_t)gridDim.x * blockDim.x)
-    s[region_index(r, (uint64_t)(off + i))] = in[i];
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = region_index(lut, r.nchunks, r.L, r.m, r.selmask, (uint64_t)(off + i));
+    if (PACK)
+      buf[i] = s[a];
+    else
+      s[a] = buf[i];
+  }
 }
 
 // dst[P(f)] = src[f]; P built from 8-bit lookup tables (kernel parameter,
@@ -107,7 +109,7 @@ int grid_for(uint64_t work, int threads) {
 }
 
 int make_region(int64_t rows, int L, const int32_t* lbits, int m, uint32_t sel, Region& r) {
-  if (m < 0 || m > L || L > 62 || rows <= 0) {
+  if (m < 0 || m > L || L > 62 || rows <= 0 || L - m > 40) {
     set_error("bad region geometry (m=%d, L=%d)", m, L);
     return SVB_EINVAL;
   }
@@ -125,9 +127,19 @@ int make_region(int64_t rows, int L, const int32_t* lbits, int m, uint32_t sel, 
     // executor.py:100-105)
     if ((sel >> (m - 1 - i)) & 1) r.selmask |= uint64_t(1) << lbits[i];
   }
-  r.nfree = 0;
+  int free_bits[64], nfree = 0;
   for (int b = 0; b < L; ++b)
-    if (!(used >> b & 1)) r.free_bits[r.nfree++] = b;
+    if (!(used >> b & 1)) free_bits[nfree++] = b;
+  r.nchunks = (nfree + 7) / 8;
+  for (int c = 0; c < r.nchunks; ++c)
+    for (int v = 0; v < 256; ++v) {
+      uint64_t d = 0;
+      for (int j = 0; j < 8; ++j) {
+        const int k = 8 * c + j;
+        if (k < nfree && ((v >> j) & 1)) d |= uint64_t(1) << free_bits[k];
+      }
+      r.lut[c * 256 + v] = d;
+    }
   return SVB_OK;
 }
 
@@ -176,8 +188,9 @@ extern "C" int svb_pack_region(const svb_c128* state, int64_t rows, int L, const
     return SVB_EINVAL;
   }
   if (!count) return SVB_OK;
-  k_pack<<<grid_for(count, 256), 256, 0, as_stream(stream)>>>(
-      reinterpret_cast<const double2*>(state), r, off, count, reinterpret_cast<double2*>(out));
+  k_region<true><<<grid_for(count, 256), 256, 0, as_stream(stream)>>>(
+      const_cast<double2*>(reinterpret_cast<const double2*>(state)), r, off, count,
+      reinterpret_cast<double2*>(out));
   SVB_CHECK_LAUNCH("svb_pack_region");
   return SVB_OK;
 }
@@ -192,8 +205,9 @@ extern "C" int svb_unpack_region(svb_c128* state, int64_t rows, int L, const int
     return SVB_EINVAL;
   }
   if (!count) return SVB_OK;
-  k_unpack<<<grid_for(count, 256), 256, 0, as_stream(stream)>>>(
-      reinterpret_cast<double2*>(state), r, off, count, reinterpret_cast<const double2*>(in));
+  k_region<false><<<grid_for(count, 256), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<double2*>(state), r, off, count,
+      const_cast<double2*>(reinterpret_cast<const double2*>(in)));
   SVB_CHECK_LAUNCH("svb_unpack_region");
   return SVB_OK;
 }

@@ -120,6 +120,13 @@ class Swap:
 
 
 @dataclass
+class ExchMark:
+    """Marker in the planning stream: these reference local bits are exchanged next."""
+
+    bits: tuple
+
+
+@dataclass
 class Factor:
     """Diagonal factor: multiply by c where every bit in `bits` is 1 (0-2 bits)."""
 
@@ -407,10 +414,14 @@ class _Lookahead:
     def __init__(self, stream: list, start: int, n_local: int):
         lab = list(range(max(n_local, 1) + 64))
         first_use: dict = {}
+        self.exchange: list = []  # current labels of the next remap's local bits
         for i in range(start, len(stream)):
             pr = stream[i]
             if isinstance(pr, Swap):
                 lab[pr.a], lab[pr.b] = lab[pr.b], lab[pr.a]
+            elif isinstance(pr, ExchMark):
+                if not self.exchange:
+                    self.exchange = [lab[b] for b in pr.bits]
             else:
                 for b in _needs(pr):
                     cur = lab[b]
@@ -430,8 +441,16 @@ def _choose_store(tile: list, where: list, look: _Lookahead, low: int, n_local: 
     dest = {p: p for p in fixed}
     free = set(p for p in tile if p in inv)
     placed: dict = {}
+    # qubits of the next remap go to the top physical bits first: contiguous
+    # regions, so the NCCL exchange needs no pack/unpack pass
+    tops = [p for p in range(n_local - 1, n_local - 1 - len(look.exchange), -1) if p in free]
+    for r in look.exchange:
+        if r in ids and tops:
+            placed[r] = tops.pop(0)
+            free.discard(placed[r])
     lows = [p for p in range(low) if p in free]
-    soon = sorted((r for r in ids if r in look.first_use), key=lambda r: look.first_use[r])
+    soon = sorted((r for r in ids if r in look.first_use and r not in placed),
+                  key=lambda r: look.first_use[r])
     for p, r in zip(lows, soon):
         placed[r] = p
     free -= set(placed.values())
@@ -491,11 +510,15 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
             for e in task.payload["gates"]:
                 prims.extend(resolve_entry(e, layout, geo))
             leaves.append((task.id, prims))
-    stream = [pr for _, prims in leaves for pr in prims]
-    leaf_start, pos = {}, 0
-    for tid, prims in leaves:
-        leaf_start[tid] = pos
-        pos += len(prims)
+    # planning stream: every leaf's primitives, with a marker per remap
+    stream, leaf_start = [], {}
+    prims_of = dict(leaves)
+    for task in plan.tasks:
+        if task.kind == "ApplyFused":
+            leaf_start[task.id] = len(stream)
+            stream.extend(prims_of[task.id])
+        elif task.kind == "Exchange":
+            stream.append(ExchMark(tuple(L - 1 - s["local_bit"] for s in task.payload["swaps"])))
 
     buf = ProgramBuffers()
     steps: list = []
@@ -557,6 +580,12 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
                 if len(tile) >= K:
                     break
                 tile.add(trial[r])
+            for r in look.exchange:  # let the store park the next remap's qubits on top
+                if len(tile) + 2 <= K:
+                    tile |= {trial[r]}
+            for p_top in range(L - 1, L - 1 - len(look.exchange), -1):
+                if len(tile) < K:
+                    tile.add(p_top)
             _pad_displaced(tile, trial, look, K, L)
             for b in range(D):
                 if len(tile) >= K:
