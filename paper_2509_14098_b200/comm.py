@@ -16,12 +16,17 @@ with the gloo backend on CPU tensors (tests/test_comm_gloo.py).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
-CHUNK_BYTES = 256 << 20  # per peer per buffer
+# NCCL send/recv on B200 NVLink is message-size bound (measured with
+# tools/nvlink_bench.py: 298 GB/s at 64 MiB, 333 at 256 MiB, 636 at 1 GiB per
+# direction), so chunks are as large as the staging budget allows.
+STAGING_BYTES = int(os.environ.get("SVB200_STAGING_BYTES", str(8 << 30)))
+MIN_CHUNK_BYTES = 256 << 20
 
 
 @dataclass
@@ -95,7 +100,8 @@ def exchange(state, remote: list, geo, group, mover=None, chunk_elems: int | Non
     peers = peer_plan(me, ebits, m)
     region = state.rows << (state.L - m)
     if chunk_elems is None:
-        chunk_elems = max(1, min(region, CHUNK_BYTES // 16))
+        nbuf_bytes = max(MIN_CHUNK_BYTES, STAGING_BYTES // (2 * max(1, len(peers))))
+        chunk_elems = max(1, min(region, nbuf_bytes // 16))
     mover = mover or CudaMover(state)
     dev = state.buf.device
     L = state.L
