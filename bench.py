@@ -193,7 +193,7 @@ def run_reference_arm(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="qft")
@@ -240,14 +240,15 @@ def main() -> None:
 
     # timed region: K full circuits, device-timed with CUDA events
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    compute_s, launches = 0.0, 0
+    compute_s, launches, sweeps = 0.0, 0, 0
     with ClockSampler(local) as clk:
         barrier()
         start.record()
         for _ in range(args.steps):
             res = run_plan(plan)
-            compute_s += res.stats.compute_seconds
+            compute_s += res.stats.compute_seconds + res.stats.layout_seconds
             launches += res.stats.kernel_launches
+            sweeps += res.stats.sweeps
         stop.record()
         barrier()
     elapsed = max_over_ranks(start.elapsed_time(stop) / 1e3)
@@ -260,8 +261,9 @@ def main() -> None:
     peak, peak_kind = peak_hbm()
     rows = (1 << plan.g) // world
     fused = sum(1 for t in plan.tasks if t.kind == "ApplyFused")
-    per_rank_sweep_bytes = fused * 32 * (rows << (plan.d - plan.g))
-    achieved = per_rank_sweep_bytes * args.steps / compute_s / 1e9
+    launch_bytes = 32 * (rows << (plan.d - plan.g))  # one read + one write of the device state
+    sweeps = int(max_over_ranks(float(sweeps)))
+    achieved = launch_bytes * sweeps / compute_s / 1e9
 
     # e2e: initial state from pinned host memory, final blocks back to pinned host
     torch.cuda.synchronize()
@@ -308,9 +310,11 @@ def main() -> None:
                         * args.steps / elapsed,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_sweep", "peak_source": f"{peak_kind} hbm_gbs",
-                     "bytes_per_launch": 32 * (rows << (plan.d - plan.g)),
-                     "launch_ms": 1e3 * compute_s / (fused * args.steps)},
+                     "kernel": "sweep (NVRTC-specialised svb_jit_*; csrc/sweep.cu interpreter on small states)",
+                     "peak_source": f"{peak_kind} hbm_gbs (copy bandwidth, burst)",
+                     "bytes_per_launch": launch_bytes,
+                     "launches_per_step": sweeps // args.steps,
+                     "launch_ms": 1e3 * compute_s / max(sweeps, 1)},
         "e2e": e2e,
         "gpu_launches": launches,
         "compile_ms": 1e3 * stats.compile_seconds,
