@@ -110,14 +110,15 @@ extern "C" int svb_jit_load(const void* image, const char* kernel_name, void** k
   e = cudaLibraryGetKernel(&k, lib, kernel_name);
   if (e != cudaSuccess) return cuda_status(e, "cudaLibraryGetKernel");
   e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(jit)");
   *kernel = reinterpret_cast<void*>(k);
   return SVB_OK;
 }
 
-// Launch a generated sweep kernel: one CTA per SM (persistent), 2^(K-4)
-// threads, two tile buffers plus per-tile slots of dynamic shared memory.
+// Launch a generated sweep kernel: one CTA per SM (persistent), 2^(K-rb)
+// threads, three rotating tile buffers plus per-tile slots of dynamic
+// shared memory.
 extern "C" int svb_jit_launch_sweep(void* kernel, svb_c128* state, const void* prog,
                                     const svb_sweep_desc* desc, double* norm_out, int grid_limit,
                                     void* stream) {
@@ -133,7 +134,7 @@ extern "C" int svb_jit_launch_sweep(void* kernel, svb_c128* state, const void* p
   int64_t grid = kNumSMs;
   if (grid_limit > 0 && grid > grid_limit) grid = grid_limit;
   if (grid > ntiles) grid = ntiles;
-  const size_t smem = sizeof(double2) * ((size_t(2) << d.K) + (size_t)d.nctab);
+  const size_t smem = sizeof(double2) * ((size_t(3) << d.K) + (size_t)d.nctab);  // 3 tile buffers
   cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(kernel), dim3((unsigned)grid),
                                    dim3(1u << (d.K - d.rb)), args, smem,
                                    as_stream(stream));

@@ -123,7 +123,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
     w("  extern __shared__ __align__(16) double2 smem[];")
     w("  __shared__ double red[32];")
     w("  const int t = threadIdx.x;")
-    w(f"  double2* const ctab = smem + {2 << K};")
+    w(f"  double2* const ctab = smem + {3 << K};")
     # per-thread constants
     w(f"  const u64 ld_t = {_deposit('t', tin[:tb])};")
     w(f"  const u32 lds_t = {_xor_img('t', sw[:tb])};")
@@ -154,9 +154,17 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
     def origin(var):
         return _deposit(var, fbits) if fbits else "0ull"
 
-    def prefetch(buf, base):
-        w("    {")
-        for it in range(NR):
+    TILE = 1 << K
+    nst = sum(1 for op in ops if int(op["kind"]) == prog.OP_STAGE)
+    nslots = max(nst, 1)
+
+    def chunks(n):  # split range(n) into nslots nearly equal consecutive parts
+        return [list(range(n * j // nslots, n * (j + 1) // nslots)) for j in range(nslots)]
+
+    pf_chunks, st_chunks = chunks(NR), chunks(NR)
+
+    def prefetch_items(buf, base, items, commit=True):
+        for it in items:
             dev = 0
             s = 0
             for q in range(rb):
@@ -164,29 +172,62 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
                     dev |= 1 << tin[tb + q]
                     s ^= sw[tb + q]
             w(f"      cp_async16({buf} + (lds_t ^ {s}u), state + ({base} | ld_t | {dev}ull));")
-        w("      cp_async_commit();")
-        w("    }")
+        if commit and items:
+            w("      cp_async_commit();")
 
+    def store_items(buf, base, items):
+        for it in items:
+            dev = 0
+            s = 0
+            for q in range(rb):
+                if (it >> q) & 1:
+                    dev |= 1 << st_dev[tb + q]
+                    s ^= st_sw[tb + q]
+            w("      {")
+            w(f"        const double2 v = {buf}[sts_t ^ {s}u];")
+            w("        nrm = fma(v.x, v.x, fma(v.y, v.y, nrm));")
+            w(f"        st_stream(state + ({base} | ((st_t | {dev}ull) ^ {st_flip}ull)), v);")
+            w("      }")
+
+    def slot(j):
+        """Issue slice j of the next tile's prefetch and of the previous tile's store."""
+        if pf_chunks[j]:
+            w("    if (has_next) {")
+            prefetch_items("nbuf", "bn", pf_chunks[j])
+            w("    }")
+        if st_chunks[j]:
+            w("    if (iter > 0) {")
+            store_items("pbuf", "bp", st_chunks[j])
+            w("    }")
+
+    # Three tile buffers rotate: tile i is computed in buffer i % 3 while the
+    # prefetch of tile i+1 and the store of tile i-1 are issued in slices
+    # between its stages, so loads, stores and FP64 work overlap.
     w(f"  if (tile_id < {ntiles}ll) {{")
     w(f"    const u64 b0 = {origin('tile_id')};")
-    prefetch("smem", "b0")
+    prefetch_items("smem", "b0", list(range(NR)))
     w("  }")
-    w(f"  for (int iter = 0; tile_id < {ntiles}ll; ++iter, tile_id += gridDim.x) {{")
-    w(f"    double2* const tile = (iter & 1) ? smem + {1 << K} : smem;")
+    w("  int iter = 0;")
+    w(f"  for (; tile_id < {ntiles}ll; ++iter, tile_id += gridDim.x) {{")
+    w("    const int r3 = iter % 3;")
+    w(f"    double2* const tile = smem + r3 * {TILE};")
+    w(f"    double2* const nbuf = smem + (r3 == 2 ? 0 : r3 + 1) * {TILE};")
+    w(f"    double2* const pbuf = smem + (r3 == 0 ? 2 : r3 - 1) * {TILE};")
     w(f"    const u64 base = {origin('tile_id')};")
+    w(f"    const bool has_next = tile_id + gridDim.x < {ntiles}ll;")
+    w("    const long long nx = tile_id + gridDim.x;")
+    w(f"    const u64 bn = {origin('nx')};")
+    w("    const long long px = tile_id - gridDim.x;")
+    w(f"    const u64 bp = {origin('px')};")
     if nct:
         w(f"    tile_slots(ctab, {nct}, cterms, cofs, base, t, {NT});")
     w("    cp_async_wait_all();")
     w("    __syncthreads();")
-    w(f"    if (tile_id + gridDim.x < {ntiles}ll) {{")
-    w("      const long long nx = tile_id + gridDim.x;")
-    w(f"      const u64 bn = {origin('nx')};")
-    w(f"      double2* const nbuf = (iter & 1) ? smem : smem + {1 << K};")
-    prefetch("nbuf", "bn")
-    w("    }")
     w(f"    double2 x[{NR}];")
 
     cur = None  # current stage index
+    if nst == 0:
+        slot(0)
     for op in ops:
         kind = int(op["kind"])
         if kind == prog.OP_STAGE:
@@ -200,6 +241,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
             for v in range(NR):
                 w(f"    x[{v}] = tile[sb{nxt} ^ {offs[v]}u];")
             cur = nxt
+            slot(nxt)
             continue
         _emit_op(w, op, coef, cur, K, rb)
 
@@ -207,19 +249,14 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
         _, _, offs = stage_info[cur]
         for v in range(NR):
             w(f"    tile[sb{cur} ^ {offs[v]}u] = x[{v}];")
-    w("    __syncthreads();")
-    for it in range(NR):
-        dev = 0
-        s = 0
-        for q in range(rb):
-            if (it >> q) & 1:
-                dev |= 1 << st_dev[tb + q]
-                s ^= st_sw[tb + q]
-        w("    {")
-        w(f"      const double2 v = tile[sts_t ^ {s}u];")
-        w("      nrm = fma(v.x, v.x, fma(v.y, v.y, nrm));")
-        w(f"      st_stream(state + (base | ((st_t | {dev}ull) ^ {st_flip}ull)), v);")
-        w("    }")
+    w("  }")
+    # the last tile of this CTA is still in shared memory
+    w("  __syncthreads();")
+    w("  if (iter > 0) {")
+    w(f"    double2* const pbuf = smem + ((iter - 1) % 3) * {TILE};")
+    w("    const long long px = tile_id - gridDim.x;")
+    w(f"    const u64 bp = {origin('px')};")
+    store_items("pbuf", "bp", list(range(NR)))
     w("  }")
     w("  cp_async_wait_all();")
     w("  if (norm_out != nullptr) {")
