@@ -12,6 +12,9 @@ import torch  # noqa: E402
 from paper_2509_14098_b200 import _native, executor, jit, plan as planmod, program as prog  # noqa: E402
 
 docs = json.load(gzip.open(ROOT / "tests/golden/grid.json.gz", "rt"))
+if len(sys.argv) > 1:  # plans/<name>.json.gz instead of the grid
+    docs = [{"name": n, "plan": json.loads(planmod.to_json(planmod.load(str(ROOT / "plans" / f"{n}.json.gz"))))}
+            for n in sys.argv[1:]]
 lib = _native.load()
 bad = 0
 for doc in docs:
@@ -20,7 +23,10 @@ for doc in docs:
         continue
     L = plan.d - plan.g
     geo = prog.DeviceGeometry(d=plan.d, g=plan.g, h=plan.g, rank_base=0, pad_to=4)
-    buf = prog.plan_device(plan, geo).buf
+    buf4 = prog.plan_device(plan, geo, rb=4).buf  # interpreter program
+    buf = prog.plan_device(plan, geo, rb=3).buf  # JIT program (same sweeps)
+    blob4, descs4, _ = prog.pack(buf4)
+    dblob4 = torch.from_numpy(blob4).cuda()
     blob, descs, _ = prog.pack(buf)
     dblob = torch.from_numpy(blob).cuda()
     names, cubins = jit.build_kernels(buf)
@@ -33,8 +39,8 @@ for doc in docs:
         a = torch.from_numpy(v.copy()).cuda()
         b = torch.from_numpy(v.copy()).cuda()
         st = torch.cuda.current_stream().cuda_stream
-        _native.check(lib.svb_run_sweeps(a.data_ptr(), 1 << (geo.D - L), L, dblob.data_ptr(),
-                                         descs[i:i + 1].ctypes.data, 1, None, 0, st), "interp")
+        _native.check(lib.svb_run_sweeps(a.data_ptr(), 1 << (geo.D - L), L, dblob4.data_ptr(),
+                                         descs4[i:i + 1].ctypes.data, 1, None, 0, st), "interp")
         _native.check(lib.svb_jit_launch_sweep(kern[i], b.data_ptr(), dblob.data_ptr(),
                                                descs[i:i + 1].ctypes.data, None, 0, st), "jit")
         torch.cuda.synchronize()
