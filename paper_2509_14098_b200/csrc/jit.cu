@@ -134,7 +134,8 @@ extern "C" int svb_jit_launch_sweep(void* kernel, svb_c128* state, const void* p
   int64_t grid = kNumSMs;
   if (grid_limit > 0 && grid > grid_limit) grid = grid_limit;
   if (grid > ntiles) grid = ntiles;
-  const size_t smem = sizeof(double2) * ((size_t(3) << d.K) + (size_t)d.nctab);  // 3 tile buffers
+  // 3 tile buffers + per-tile slots double-buffered by tile parity
+  const size_t smem = sizeof(double2) * ((size_t(3) << d.K) + 2 * (size_t)(d.nctab > 0 ? d.nctab : 1));
   cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(kernel), dim3((unsigned)grid),
                                    dim3(1u << (d.K - d.rb)), args, smem,
                                    as_stream(stream));

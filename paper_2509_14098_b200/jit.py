@@ -123,7 +123,10 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
     w("  extern __shared__ __align__(16) double2 smem[];")
     w("  __shared__ double red[32];")
     w("  const int t = threadIdx.x;")
-    w(f"  double2* const ctab = smem + {3 << K};")
+    # per-tile slots are double-buffered by tile parity: the next tile's slots
+    # are written while slow warps may still read this tile's (no barrier
+    # between consecutive tiles)
+    w(f"  double2* const ctab_base = smem + {3 << K};")
     # per-thread constants
     w(f"  const u64 ld_t = {_deposit('t', tin[:tb])};")
     w(f"  const u32 lds_t = {_xor_img('t', sw[:tb])};")
@@ -214,6 +217,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
     w(f"    double2* const nbuf = smem + (r3 == 2 ? 0 : r3 + 1) * {TILE};")
     w(f"    double2* const pbuf = smem + (r3 == 0 ? 2 : r3 - 1) * {TILE};")
     w(f"    const u64 base = {origin('tile_id')};")
+    w(f"    double2* const ctab = ctab_base + (iter & 1) * {max(nct, 1)};")
     w(f"    const bool has_next = tile_id + gridDim.x < {ntiles}ll;")
     w("    const long long nx = tile_id + gridDim.x;")
     w(f"    const u64 bn = {origin('nx')};")
