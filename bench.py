@@ -292,7 +292,8 @@ def main() -> None:
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(name)
+            entry = json.loads(prof.read_text()).get(name)
+            traffic = entry["bytes_per_launch"] if entry else None
         except Exception:
             traffic = None
 
