@@ -224,7 +224,24 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
     w("    const long long px = tile_id - gridDim.x;")
     w(f"    const u64 bp = {origin('px')};")
     if nct:
-        w(f"    tile_slots(ctab, {nct}, cterms, cofs, base, t, {NT});")
+        lut_off, nch = int(desc["lut_off"]), int(desc["lut_nch"])
+        residual = desc["residual"]
+        w(f"    for (int i = t; i < {nct}; i += {NT}) {{")
+        w(f"      const double2* lt = tab + {lut_off} + i * {nch * 256};")
+        w("      double2 acc = __ldg(lt + (tile_id & 255));")
+        for c in range(1, nch):
+            w(f"      acc = cmul(acc, __ldg(lt + {c * 256} + ((tile_id >> {8 * c}) & 255)));")
+        if any(residual):
+            for s_, terms in enumerate(residual):
+                if not terms:
+                    continue
+                w(f"      if (i == {s_}) {{")
+                for mask, cval in terms:
+                    w(f"        if ((base & {int(mask)}ull) == {int(mask)}ull) "
+                      f"acc = cmulc(acc, {_lit(cval.real)}, {_lit(cval.imag)});")
+                w("      }")
+        w("      ctab[i] = acc;")
+        w("    }")
     w("    cp_async_wait_all();")
     w("    __syncthreads();")
     w(f"    double2 x[{NR}];")
@@ -281,12 +298,24 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
 
 
 def _phase_base(w, op, coef_c0: complex, K: int, rb: int) -> None:
-    """Emit `p` = const * per-tile slot * per-thread table * per-thread-bit slots."""
-    w(f"      double2 p = make_double2({_lit(coef_c0.real)}, {_lit(coef_c0.imag)});")
+    """Emit `p` = const * per-tile slot * per-thread table * per-thread-bit slots.
+
+    A unit constant is not multiplied (x * 1 is not folded by the compiler
+    under IEEE rules)."""
+    factors = []
     if int(op["ctab"]) >= 0:
-        w(f"      p = cmul(p, ctab[{int(op['ctab'])}]);")
+        factors.append(f"ctab[{int(op['ctab'])}]")
     if int(op["tab"]) >= 0:
-        w(f"      p = cmul(p, tab{int(op['tab'])});")
+        factors.append(f"tab{int(op['tab'])}")
+    c0 = complex(coef_c0)
+    if not factors:
+        w(f"      double2 p = make_double2({_lit(c0.real)}, {_lit(c0.imag)});")
+    else:
+        w(f"      double2 p = {factors[0]};")
+        for f in factors[1:]:
+            w(f"      p = cmul(p, {f});")
+        if c0 != 1:
+            w(f"      p = {_cmul_lit('p', c0)};")
     if int(op["tf"]) >= 0:
         for i in range(K - rb):
             w(f"      if ((t >> {i}) & 1) p = cmul(p, ctab[{int(op['tf']) + i}]);")

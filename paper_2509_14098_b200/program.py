@@ -909,6 +909,32 @@ def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers, rb: i
         offs.append(len(buf.cterms))
     buf.cofs.extend(offs)
 
+    # the same terms as 8-bit lookup tables over the tile index (generated
+    # kernels): slot s = prod_c LUT[s][c][(tile_id >> 8c) & 255], plus the
+    # rare terms whose bits span two chunks
+    fbits = [b for b in range(geo.D) if b not in dev_to_tile]
+    fpos = {b: i for i, b in enumerate(fbits)}
+    nch = max(1, (len(fbits) + 7) // 8)
+    lut_off, residual = -1, []
+    if nct[0]:
+        lut = np.ones((nct[0], nch, 256), dtype=np.complex128)
+        vals = np.arange(256)
+        for s_ in range(nct[0]):
+            res_s = []
+            for mask, c in ctab_terms[s_]:
+                idx = [fpos[b] for b in range(geo.D) if (mask >> b) & 1]
+                chunks_ = {i // 8 for i in idx}
+                if not idx:
+                    lut[s_, 0, :] *= c
+                elif len(chunks_) == 1:
+                    k = chunks_.pop()
+                    lm = sum(1 << (i - 8 * k) for i in idx)
+                    lut[s_, k, (vals & lm) == lm] *= c
+                else:
+                    res_s.append((mask, c))
+            residual.append(res_s)
+        lut_off = buf.add_tab(lut.reshape(-1))
+
     tout = [sp.out_map[tin[k]][0] for k in range(K)]
     st_flip = 0
     for k in range(K):
@@ -919,6 +945,7 @@ def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers, rb: i
         st_dev=[tout[k] for k in store_order], st_sw=[sw[k] for k in store_order],
         st_flip=st_flip, op_begin=op_begin, op_count=op_count, nctab=nct[0],
         norm_slot=sp.norm_slot, cofs_index=cofs_base, rb=rb,
+        lut_off=lut_off, lut_nch=nch, residual=residual,
     )
     buf.descs.append(desc)
 
