@@ -119,18 +119,23 @@ class _Compiled:
     host_blob: np.ndarray = field(repr=False, default=None)
     kernels: list | None = None  # per-descriptor JIT kernel handles (None: interpreter)
     jit_seconds: float = 0.0
+    zero_init: dict = field(default_factory=dict)  # descriptors that synthesise |0...0>
     n_sweeps: int = 0
 
 
 _compile_cache: dict = {}
 
 
-def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None) -> _Compiled:
-    """Compile every ApplyFused task of the plan for this device (cached)."""
+def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: bool = False) -> _Compiled:
+    """Compile every ApplyFused task of the plan for this device (cached).
+
+    zero_start: the run starts from |0...0>, so the first sweep (if no remap
+    precedes it) synthesises its tiles instead of reading a zeroed state."""
     import time
 
     use_jit = _use_jit(geo, jit)
-    key = (id(plan), len(plan.tasks), geo.d, geo.g, geo.h, geo.rank_base, str(device), use_jit)
+    key = (id(plan), len(plan.tasks), geo.d, geo.g, geo.h, geo.rank_base, str(device), use_jit,
+           zero_start)
     hit = _compile_cache.get(key)
     if hit is not None and hit[0] is plan:
         return hit[1]
@@ -148,7 +153,16 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None) -> _Compiled:
         from . import jit as jitmod
 
         t1 = time.perf_counter()
-        names, cubins = jitmod.build_kernels(dp.buf)
+        zinit = {}
+        if zero_start:
+            for st in dp.steps:
+                if st.kind == "exchange":
+                    break
+                if st.kind == "sweeps" and st.count:
+                    zinit[st.first] = 1 if geo.rank_base == 0 else 2
+                    break
+        names, cubins = jitmod.build_kernels(dp.buf, zero_init=zinit)
+        out.zero_init = dict(jitmod._LAST_ZERO_INIT)
         dev_index = device.index if device.index is not None else torch.cuda.current_device()
         out.kernels = [jitmod.load_kernel(n, c, dev_index) for n, c in zip(names, cubins)]
         out.jit_seconds = time.perf_counter() - t1
@@ -182,10 +196,11 @@ def _bitperm(src: torch.Tensor, dst: torch.Tensor, perm: list) -> None:
 class _State:
     """Device storage with a phantom pad so tiny states still fill 16 amplitudes."""
 
-    def __init__(self, rows: int, L: int, device):
+    def __init__(self, rows: int, L: int, device, zero: bool = True):
         self.rows, self.L = rows, L
         n = rows << L
-        self.buf = torch.zeros(max(n, prog.NREG), dtype=torch.complex128, device=device)
+        alloc = torch.zeros if zero else torch.empty
+        self.buf = alloc(max(n, prog.NREG), dtype=torch.complex128, device=device)
         self.blocks = self.buf[:n].view(rows, 1 << L)
 
 
@@ -262,11 +277,12 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 fail(PlanInvalid("double Alloc"))
             if task.payload["num_ranks"] != nranks or task.payload["block_len"] != 1 << L:
                 fail(PlanInvalid("Alloc payload disagrees with plan shape"))
-            state = _State(rows, L, device)
-            compiled = compile_plan(plan, geo_eff, device, jit)
+            compiled = compile_plan(plan, geo_eff, device, jit, zero_start=initial is None)
             stats.compile_seconds = compiled.compile_seconds + compiled.jit_seconds
+            # when the first sweep synthesises |0...0> the state needs no memset
+            state = _State(rows, L, device, zero=not compiled.zero_init)
             if initial is None:
-                if rank_base == 0:
+                if rank_base == 0 and not compiled.zero_init:
                     state.blocks[0, 0] = 1.0  # |0...0> sits at index 0 in every layout
             else:
                 full = scatter(initial, plan, phase=0, device=device, local_perm=compiled.init_perm[:L])
@@ -282,6 +298,8 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 _run_descs(compiled, st.first, st.count, state, rows_eff, L, norms, grid_limit, stream)
             elif slot > 0:  # relabel-only leaf: the state (and its norm) is unchanged
                 norms[slot:slot + 1].copy_(norms[slot - 1:slot])
+            elif initial is None:  # |0...0> (possibly not materialised yet) has norm 1
+                norms[0:1].fill_(1.0 / world)
             else:
                 lib.svb_norm2(state.buf.data_ptr(), rows << L, norms[slot:].data_ptr(), stream)
             count = st.count

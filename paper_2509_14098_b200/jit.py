@@ -99,7 +99,12 @@ def _xor_img(var: str, imgs) -> str:
 # kernel generator
 # ---------------------------------------------------------------------------
 
-def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
+def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int = 0) -> str:
+    """Straight-line kernel for one sweep.
+
+    zero_init: 0 = load the state; 1 = the input is |0...0> with the unit
+    amplitude on this device (synthesise tiles, no loads); 2 = the input is
+    all zeros on this device."""
     K, D = desc["K"], desc["D"]
     rb = int(desc.get("rb", prog.RB)) if hasattr(desc, "get") else int(desc["rb"])
     NR = 1 << rb
@@ -194,7 +199,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
 
     def slot(j):
         """Issue slice j of the next tile's prefetch and of the previous tile's store."""
-        if pf_chunks[j]:
+        if pf_chunks[j] and not zero_init:
             w("    if (has_next) {")
             prefetch_items("nbuf", "bn", pf_chunks[j])
             w("    }")
@@ -206,10 +211,11 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
     # Three tile buffers rotate: tile i is computed in buffer i % 3 while the
     # prefetch of tile i+1 and the store of tile i-1 are issued in slices
     # between its stages, so loads, stores and FP64 work overlap.
-    w(f"  if (tile_id < {ntiles}ll) {{")
-    w(f"    const u64 b0 = {origin('tile_id')};")
-    prefetch_items("smem", "b0", list(range(NR)))
-    w("  }")
+    if not zero_init:
+        w(f"  if (tile_id < {ntiles}ll) {{")
+        w(f"    const u64 b0 = {origin('tile_id')};")
+        prefetch_items("smem", "b0", list(range(NR)))
+        w("  }")
     w("  int iter = 0;")
     w(f"  for (; tile_id < {ntiles}ll; ++iter, tile_id += gridDim.x) {{")
     w("    const int r3 = iter % 3;")
@@ -259,8 +265,15 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list) -> str:
                     w(f"    tile[sb{cur} ^ {offs[v]}u] = x[{v}];")
                 w("    __syncthreads();")
             _, _, offs = stage_info[nxt]
-            for v in range(NR):
-                w(f"    x[{v}] = tile[sb{nxt} ^ {offs[v]}u];")
+            if nxt == 0 and zero_init:
+                # |0...0>: every amplitude is zero except index 0 of the device
+                for v in range(NR):
+                    w(f"    x[{v}] = make_double2(0.0, 0.0);")
+                if zero_init == 1:
+                    w("    if (base == 0ull && t == 0) x[0] = make_double2(1.0, 0.0);")
+            else:
+                for v in range(NR):
+                    w(f"    x[{v}] = tile[sb{nxt} ^ {offs[v]}u];")
             cur = nxt
             slot(nxt)
             continue
@@ -417,6 +430,7 @@ def _emit_dfs(w, a: int, nt: int, c: list, fused_h: bool, rb: int) -> None:
 # ---------------------------------------------------------------------------
 
 _mem_cache: dict = {}  # source hash -> cubin bytes
+_LAST_ZERO_INIT: dict = {}  # descriptors the last build_kernels synthesised from |0>
 _kernels: dict = {}  # (source hash, device) -> kernel handle
 
 
@@ -463,6 +477,11 @@ def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: in
         name = f"{prefix}_{h}"
         srcs.append(body.replace("KNAME", name))
         names.append(name)
+    _LAST_ZERO_INIT.clear()
+    _LAST_ZERO_INIT.update({i: z for i, z in zero_init.items()
+                            if any(int(o["kind"]) == prog.OP_STAGE
+                                   for o in buf.ops[buf.descs[i]["op_begin"]:
+                                                    buf.descs[i]["op_begin"] + buf.descs[i]["op_count"]])})
     threads = threads or min(32, os.cpu_count() or 4)
     with ThreadPoolExecutor(max_workers=threads) as ex:
         cubins = list(ex.map(lambda sn: _compile(*sn), zip(srcs, names)))
