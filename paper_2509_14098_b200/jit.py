@@ -466,22 +466,29 @@ def _compile(src: str, name: str) -> bytes:
     return data
 
 
-def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: int | None = None):
-    """One kernel per descriptor; register-slot count per sweep comes from the descriptor."""
-    """Generate + compile one kernel per sweep descriptor; returns (names, cubins, hashes)."""
+def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: int | None = None,
+                  zero_init: dict | None = None):
+    """Generate + compile one kernel per sweep descriptor; returns (names, cubins).
+
+    zero_init maps descriptor index -> 1/2 for sweeps whose input is known to
+    be |0...0> (see kernel_source); _LAST_ZERO_INIT records which were used."""
     srcs, names = [], []
+    zero_init = zero_init or {}
+    used = {}
     for i, d in enumerate(buf.descs):
         ops = buf.ops[d["op_begin"]: d["op_begin"] + d["op_count"]]
-        body = kernel_source("KNAME", d, ops, buf.coef)
+        zi = zero_init.get(i, 0)
+        if zi and not any(int(o["kind"]) == prog.OP_STAGE for o in ops):
+            zi = 0  # no register stage to synthesise into
+        if zi:
+            used[i] = zi
+        body = kernel_source("KNAME", d, ops, buf.coef, zi)
         h = hashlib.sha1(body.encode()).hexdigest()[:16]
         name = f"{prefix}_{h}"
         srcs.append(body.replace("KNAME", name))
         names.append(name)
     _LAST_ZERO_INIT.clear()
-    _LAST_ZERO_INIT.update({i: z for i, z in zero_init.items()
-                            if any(int(o["kind"]) == prog.OP_STAGE
-                                   for o in buf.ops[buf.descs[i]["op_begin"]:
-                                                    buf.descs[i]["op_begin"] + buf.descs[i]["op_count"]])})
+    _LAST_ZERO_INIT.update(used)
     threads = threads or min(32, os.cpu_count() or 4)
     with ThreadPoolExecutor(max_workers=threads) as ex:
         cubins = list(ex.map(lambda sn: _compile(*sn), zip(srcs, names)))
