@@ -111,6 +111,16 @@ class Dense1:
     m: np.ndarray
     ctrl: dict  # device bit -> required value (0/1)
     noop: bool = False  # a constant-0 control made it identity on this device
+    perm: bool = False  # structurally a bit flip (x, cx, ccx): costs no FP64
+
+
+@dataclass
+class Dense2:
+    """4x4 on device bits (a, b); matrix index bit 1 <-> a, bit 0 <-> b."""
+
+    a: int
+    b: int
+    m: np.ndarray
 
 
 @dataclass
@@ -222,12 +232,11 @@ def resolve_entry(entry: dict, layout, geo: DeviceGeometry) -> list:
         sub = np.asarray(diag[idx]).reshape(-1)
         return _decompose_diag(sub, [slot_bit[i] for i in free])
 
-    # non-diagonal: fixed slots are controls (validated above)
-    if any(slot_const[i] == 0 for i in fixed):
-        # identity on this device; kept as a placeholder so every device plans
-        # the same tiles and layouts
-        tgt = [slot_bit[i] for i in free if i not in gate.controls]
-        return [Dense1(tgt[0], np.eye(2, dtype=np.complex128), {}, noop=True)] if tgt else []
+    # non-diagonal: fixed slots are controls (validated above); a constant-0
+    # control makes the gate the identity on this device, but it is kept as a
+    # placeholder with the same structure so every device plans the same
+    # tiles, fusions and layouts
+    noop = any(slot_const[i] == 0 for i in fixed)
     m = np.asarray(gate.matrix).reshape((2,) * (2 * p))
     idx = [slice(None)] * (2 * p)
     for i in fixed:
@@ -239,12 +248,18 @@ def resolve_entry(entry: dict, layout, geo: DeviceGeometry) -> list:
     ctl = [j for j, i in enumerate(free) if i in gate.controls]
     tgt = [j for j in range(k) if j not in ctl]
     if k == 2 and not ctl and gate.kind == "swap":
+        if noop:
+            raise PlanInvalid(f"swap on {qubits} has a global slot")
         return [Swap(free_bits[0], free_bits[1])]
     block = _controlled_split(sub, ctl, k) if ctl else None
     if block is not None and len(tgt) == 1:
-        return [Dense1(free_bits[tgt[0]], block, {free_bits[j]: 1 for j in ctl})]
+        perm = bool(np.array_equal(block, _X))
+        return [Dense1(free_bits[tgt[0]], np.eye(2, dtype=np.complex128) if noop else block,
+                       {} if noop else {free_bits[j]: 1 for j in ctl}, noop=noop, perm=perm)]
     if k == 1:
-        return [Dense1(free_bits[0], sub, {})]
+        perm = bool(np.array_equal(sub, _X))
+        return [Dense1(free_bits[0], np.eye(2, dtype=np.complex128) if noop else sub, {},
+                       noop=noop, perm=perm)]
     raise NotImplementedError(f"no device decomposition for {gate.kind} on {k} free slots")
 
 
@@ -282,7 +297,107 @@ def _needs(prim) -> list:
     """Reference bits a primitive needs inside the tile (dense targets, virtual flips)."""
     if isinstance(prim, Dense1):
         return [prim.bit]
+    if isinstance(prim, Dense2):
+        return [prim.a, prim.b]
     return []
+
+
+# ---------------------------------------------------------------------------
+# 1b. gate fusion (structural, identical on every device)
+# ---------------------------------------------------------------------------
+
+
+def _embed2(pr, a: int, b: int) -> np.ndarray:
+    """4x4 of a Dense1 / Factor acting inside the bit pair (a = index bit 1)."""
+    pos = {a: 1, b: 0}
+    out = np.zeros((4, 4), dtype=np.complex128)
+    if isinstance(pr, Factor):
+        d = np.ones(4, dtype=np.complex128)
+        for i in range(4):
+            if all((i >> pos[x]) & 1 for x in pr.bits):
+                d[i] = pr.c
+        return np.diag(d)
+    if pr.noop:
+        return np.eye(4, dtype=np.complex128)
+    tb = pos[pr.bit]
+    for i in range(4):
+        if not all(((i >> pos[c]) & 1) == v for c, v in pr.ctrl.items()):
+            out[i, i] = 1
+            continue
+        ti = (i >> tb) & 1
+        for tj in range(2):
+            j = (i & ~(1 << tb)) | (tj << tb)
+            out[i, j] = pr.m[ti, tj]
+    return out
+
+
+def _bits_of(pr) -> set:
+    if isinstance(pr, Dense1):
+        return {pr.bit} | set(pr.ctrl)
+    if isinstance(pr, Dense2):
+        return {pr.a, pr.b}
+    if isinstance(pr, Factor):
+        return set(pr.bits)
+    if isinstance(pr, Swap):
+        return {pr.a, pr.b}
+    return set()
+
+
+def fuse_prims(prims: list) -> list:
+    """Merge runs of gates confined to one qubit pair into a single 4x4 (e.g.
+    the u,u,cx,u,u,cx,u,u,cx,u,u form of an SU(4)).
+
+    Blocks on disjoint pairs stay open concurrently (gates on disjoint bits
+    commute).  A block is fused when it holds at least two non-permutation
+    dense gates; otherwise its gates are emitted unchanged (phases and bit
+    flips are cheaper than a 4x4).  The decision depends only on gate
+    structure, never on device-specific constants.
+    """
+    out: list = []
+    blocks: list = []  # open blocks: dict(bits=set, prims=list)
+
+    def close(blk):
+        blocks.remove(blk)
+        ps = blk["prims"]
+        dense = [p for p in ps if isinstance(p, Dense1)]
+        nonperm = [p for p in dense if not p.perm]
+        bits = sorted(blk["bits"])
+        if len(nonperm) >= 2 and len(bits) == 2:
+            a, b = bits[1], bits[0]
+            m = np.eye(4, dtype=np.complex128)
+            for p in ps:
+                m = _embed2(p, a, b) @ m
+            out.append(Dense2(a, b, m))
+        elif len(nonperm) >= 2 and len(bits) == 1 and all(not p.ctrl for p in dense):
+            (x,) = bits
+            m = np.eye(2, dtype=np.complex128)
+            for p in ps:
+                if isinstance(p, Factor):
+                    g = np.diag([1, p.c]) if p.bits else np.eye(2) * p.c
+                else:
+                    g = np.eye(2, dtype=np.complex128) if p.noop else p.m
+                m = g @ m
+            out.append(Dense1(x, m, {}))
+        else:
+            out.extend(ps)
+
+    for pr in prims:
+        bits = _bits_of(pr)
+        fusable = isinstance(pr, (Dense1, Factor)) and len(bits) <= 2 and bits
+        hit = [blk for blk in blocks if blk["bits"] & bits]
+        if fusable and len(hit) == 1 and len(hit[0]["bits"] | bits) <= 2:
+            hit[0]["bits"] |= bits
+            hit[0]["prims"].append(pr)
+            continue
+        for blk in hit:
+            close(blk)
+        if fusable and (isinstance(pr, Dense1) or len(bits) == 2):
+            blocks.append({"bits": set(bits), "prims": [pr]})
+        else:
+            out.append(pr)
+    for blk in list(blocks):
+        close(blk)
+    return out
 
 
 def build_sweep(prims: list, tile: list, where: list) -> SweepProgram:
@@ -345,6 +460,30 @@ def build_sweep(prims: list, tile: list, where: list) -> SweepProgram:
             continue
         if isinstance(pr, Swap):
             where[pr.a], where[pr.b] = where[pr.b], where[pr.a]
+            continue
+        if isinstance(pr, Dense2):
+            pa, pb2 = where[pr.a], where[pr.b]
+            m = pr.m
+            fa, fb = pflip[pa], pflip[pb2]
+            if fa or fb:  # conjugate by the pending bit flips
+                xa = _X if fa else _I2
+                xb = _X if fb else _I2
+                f4 = np.kron(xa, xb)
+                m = f4 @ m @ f4
+            fl = flush(pa) + flush(pb2)
+            inside = [f for f in fl if set(f.bits) <= {pa, pb2}]
+            for f in fl:
+                if f not in inside:
+                    anchor = pa if pa in f.bits else pb2
+                    items.append(_Item(OP_PH, (tile_pos[anchor],), factors=[f]))
+            for f in inside:  # phases on the pair are absorbed into the 4x4
+                d = np.ones(4, dtype=np.complex128)
+                for i in range(4):
+                    bitv = {pa: (i >> 1) & 1, pb2: i & 1}
+                    if all(bitv[x] for x in f.bits):
+                        d[i] = f.c
+                m = m @ np.diag(d)
+            items.append(_Item(OP_U2, (tile_pos[pa], tile_pos[pb2]), m=np.array(m)))
             continue
         assert isinstance(pr, Dense1)
         if pr.noop:
@@ -488,7 +627,7 @@ def _pad_displaced(tile: set, where: list, look: _Lookahead, K: int, L: int) -> 
 
 
 def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_BITS,
-                max_materialize: int = 64, rb: int = RB) -> DeviceProgram:
+                max_materialize: int = 64, rb: int = RB, fuse: bool = True) -> DeviceProgram:
     """Compile every ApplyFused task of a plan for one device, with a global layout.
 
     The physical layout is a permutation `where` of the local bits that the
@@ -509,7 +648,7 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
             prims = []
             for e in task.payload["gates"]:
                 prims.extend(resolve_entry(e, layout, geo))
-            leaves.append((task.id, prims))
+            leaves.append((task.id, fuse_prims(prims) if fuse else prims))
     # planning stream: every leaf's primitives, with a marker per remap
     stream, leaf_start = [], {}
     prims_of = dict(leaves)
