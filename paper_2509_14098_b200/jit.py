@@ -122,6 +122,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     L = []
     w = L.append
     w('#include "sweep_jit.cuh"')
+    w(f"// prefetch={os.environ.get('SVB200_JIT_PREFETCH', 'early')}")
     w(f'extern "C" __global__ void __launch_bounds__({NT}, 1)')
     w(f"{name}(double2* __restrict__ state, const double2* __restrict__ tab, "
       "const svb_cterm* __restrict__ cterms, const int* __restrict__ cofs, double* __restrict__ norm_out) {")
@@ -169,7 +170,14 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     def chunks(n):  # split range(n) into nslots nearly equal consecutive parts
         return [list(range(n * j // nslots, n * (j + 1) // nslots)) for j in range(nslots)]
 
-    pf_chunks, st_chunks = chunks(NR), chunks(NR)
+    # the whole prefetch of tile i+1 goes out at the start of tile i (a full
+    # tile of latency slack); the stores of tile i-1 are spread over the stages
+    pf_mode = os.environ.get("SVB200_JIT_PREFETCH", "early")
+    if pf_mode == "spread":
+        pf_chunks = chunks(NR)
+    else:
+        pf_chunks = [list(range(NR))] + [[] for _ in range(nslots - 1)]
+    st_chunks = chunks(NR)
 
     def prefetch_items(buf, base, items, commit=True):
         for it in items:
