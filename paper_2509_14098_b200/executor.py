@@ -94,9 +94,11 @@ def _dist_info(group=None):
 
 
 JIT_MIN_D = int(os.environ.get("SVB200_JIT_MIN_D", "16"))
-# register slots per thread in generated kernels: 3 -> 2^(K-3) = 512 threads of
-# 8 amplitudes (16 warps/SM) hides FP64 latency better than 256 x 16
-JIT_REG_BITS = int(os.environ.get("SVB200_JIT_RB", "3"))
+# register slots per thread in generated kernels.  4 (256 threads x 16
+# amplitudes) needs one shared-memory round trip per 4 dense qubits instead of
+# per 3; with the 3-buffer rotation it measured 24.0 vs 27.4 ms on QFT-30 and
+# 1.28 vs 1.38 s on QV-30 (B200, round 1)
+JIT_REG_BITS = int(os.environ.get("SVB200_JIT_RB", "4"))
 
 
 def _use_jit(geo: prog.DeviceGeometry, jit) -> bool:
