@@ -195,6 +195,14 @@ int svb_jit_load(const void* image, const char* kernel_name, void** kernel);
 int svb_jit_launch_sweep(void* kernel, svb_c128* state, const void* prog,
                          const svb_sweep_desc* desc, double* norm_out, int grid_limit,
                          void* stream);
+/* Part launch: only the tiles whose chunk bits (compiled into the kernel)
+ * read part_val (device-index bits); part_tid is the same value in
+ * tile-index coordinates, ntiles the number of tiles in the part.  Lets a
+ * sweep run in parts that overlap a remap on another stream. */
+int svb_jit_launch_sweep_part(void* kernel, svb_c128* state, const void* prog,
+                              const svb_sweep_desc* desc, double* norm_out, int grid_limit,
+                              uint64_t part_val, uint64_t part_tid, int64_t ntiles,
+                              void* stream);
 
 #ifdef __cplusplus
 }

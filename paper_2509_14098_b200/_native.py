@@ -44,6 +44,8 @@ _SIGS = {
     "svb_jit_free": ([_vp], None),
     "svb_jit_load": ([_c.c_char_p, _c.c_char_p, _c.POINTER(_vp)], _int),
     "svb_jit_launch_sweep": ([_vp, _vp, _vp, _vp, _vp, _int, _vp], _int),
+    "svb_jit_launch_sweep_part": ([_vp, _vp, _vp, _vp, _vp, _int, _c.c_uint64, _c.c_uint64, _i64, _vp],
+                                  _int),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -85,19 +85,26 @@ def _as_real(t: torch.Tensor) -> torch.Tensor:
     return torch.view_as_real(t).reshape(-1) if t.is_complex() else t
 
 
-def exchange(state, remote: list, geo, group, mover=None, chunk_elems: int | None = None) -> int:
+def exchange(state, remote: list, geo, group, mover=None, chunk_elems: int | None = None,
+             cbits: list | None = None, cval: int = 0) -> int:
     """Run one inter-process exchange; returns the number of kernel launches issued.
 
     `remote` lists (device-id bit, local device bit) pairs; `state` has
-    .rows, .L and a flat complex128 `.buf` of rows * 2^L amplitudes.
+    .rows, .L and a flat complex128 `.buf` of rows * 2^L amplitudes.  With
+    `cbits` only the part of every region whose chunk bits read `cval`
+    (cbits[0] is its most significant bit) is exchanged, so a remap can be
+    split into parts that overlap the sweeps around it.
     """
     import torch.distributed as dist
 
     me = dist.get_rank(group)
     m = len(remote)
     ebits = [e for e, _ in remote]
-    lbits = [lb for _, lb in remote]
-    peers = peer_plan(me, ebits, m)
+    cbits = list(cbits or [])
+    k = len(cbits)
+    lbits = [lb for _, lb in remote] + cbits
+    peers = [PeerPlan(pp.peer, (pp.sel << k) | cval) for pp in peer_plan(me, ebits, m)]
+    m = m + k  # selector width over lbits
     region = state.rows << (state.L - m)
     if chunk_elems is None:
         nbuf_bytes = max(MIN_CHUNK_BYTES, STAGING_BYTES // (2 * max(1, len(peers))))

@@ -118,10 +118,13 @@ extern "C" int svb_jit_load(const void* image, const char* kernel_name, void** k
 
 // Launch a generated sweep kernel: one CTA per SM (persistent), 2^(K-rb)
 // threads, three rotating tile buffers plus per-tile slots of dynamic
-// shared memory.
-extern "C" int svb_jit_launch_sweep(void* kernel, svb_c128* state, const void* prog,
-                                    const svb_sweep_desc* desc, double* norm_out, int grid_limit,
-                                    void* stream) {
+// shared memory.  A "part" launch covers only the tiles whose chunk bits
+// (compiled into the kernel) read part_val; ntiles counts those tiles and
+// part_tid is part_val in tile-index coordinates (per-tile slot tables).
+extern "C" int svb_jit_launch_sweep_part(void* kernel, svb_c128* state, const void* prog,
+                                         const svb_sweep_desc* desc, double* norm_out,
+                                         int grid_limit, uint64_t part_val, uint64_t part_tid,
+                                         int64_t ntiles, void* stream) {
   const svb_sweep_desc& d = *desc;
   const char* pb = static_cast<const char*>(prog);
   const double2* tab = reinterpret_cast<const double2*>(pb + d.tab_off);
@@ -129,16 +132,27 @@ extern "C" int svb_jit_launch_sweep(void* kernel, svb_c128* state, const void* p
   const int32_t* cofs = reinterpret_cast<const int32_t*>(pb + d.cofs_off);
   double2* st = reinterpret_cast<double2*>(state);
   double* nrm = (norm_out && d.norm_slot >= 0) ? norm_out + d.norm_slot : nullptr;
-  void* args[] = {&st, &tab, &ct, &cofs, &nrm};
-  const int64_t ntiles = int64_t(1) << (d.D - d.K);
+  long long nt = ntiles;
+  void* args[] = {&st, &tab, &ct, &cofs, &nrm, &part_val, &part_tid, &nt};
   int64_t grid = kNumSMs;
   if (grid_limit > 0 && grid > grid_limit) grid = grid_limit;
   if (grid > ntiles) grid = ntiles;
+  if (grid <= 0) return SVB_OK;
   // 3 tile buffers + per-tile slots double-buffered by tile parity
   const size_t smem = sizeof(double2) * ((size_t(3) << d.K) + 2 * (size_t)(d.nctab > 0 ? d.nctab : 1));
+  if (smem > 220 * 1024) {
+    set_error("jit sweep: %zu bytes of shared memory exceed the 220 KB budget", smem);
+    return SVB_ERANGE;
+  }
   cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(kernel), dim3((unsigned)grid),
-                                   dim3(1u << (d.K - d.rb)), args, smem,
-                                   as_stream(stream));
+                                   dim3(1u << (d.K - d.rb)), args, smem, as_stream(stream));
   if (e != cudaSuccess) return cuda_status(e, "jit sweep launch");
   return SVB_OK;
+}
+
+extern "C" int svb_jit_launch_sweep(void* kernel, svb_c128* state, const void* prog,
+                                    const svb_sweep_desc* desc, double* norm_out, int grid_limit,
+                                    void* stream) {
+  return svb_jit_launch_sweep_part(kernel, state, prog, desc, norm_out, grid_limit, 0, 0,
+                                   int64_t(1) << (desc->D - desc->K), stream);
 }

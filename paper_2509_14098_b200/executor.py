@@ -119,6 +119,7 @@ class _Compiled:
     n_fused: int
     compile_seconds: float
     host_blob: np.ndarray = field(repr=False, default=None)
+    overlap: dict = field(default_factory=dict)  # descriptor -> overlapped exchange step
     kernels: list | None = None  # per-descriptor JIT kernel handles (None: interpreter)
     jit_seconds: float = 0.0
     zero_init: dict = field(default_factory=dict)  # descriptors that synthesise |0...0>
@@ -142,15 +143,24 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
     if hit is not None and hit[0] is plan:
         return hit[1]
     t0 = time.perf_counter()
-    dp = prog.plan_device(plan, geo, rb=JIT_REG_BITS if use_jit else prog.RB)
+    dist_run = _dist_info()[1] > 1
+    dp = prog.plan_device(plan, geo, rb=JIT_REG_BITS if use_jit else prog.RB,
+                          overlap_bits=OVERLAP_BITS if (use_jit and dist_run) else 0)
     blob, descs, _ = prog.pack(dp.buf)
     host = np.ascontiguousarray(blob)
     dev_blob = torch.from_numpy(host).to(device)
     steps = {}
     for st in dp.steps:
         steps[st.task_id] = st
+    # sweeps launched in parts around an overlapped remap
+    overlap = {}  # descriptor -> exchange step
+    for st in dp.steps:
+        if st.kind == "exchange" and st.cbits and all(ib >= geo.h for ib, _ in st.swaps):
+            overlap[st.pre] = st
+            overlap[st.post] = st
     out = _Compiled(dev_blob, descs, steps, dp.init_perm, dp.n_fused, time.perf_counter() - t0,
                     host, n_sweeps=len(dp.buf.descs))
+    out.overlap = overlap if use_jit else {}
     if use_jit and dp.buf.descs:
         from . import jit as jitmod
 
@@ -171,6 +181,10 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
     _compile_cache.clear()  # keep one plan resident
     _compile_cache[key] = (plan, out)
     return out
+
+
+def _has_remote(st, geo) -> bool:
+    return any(ib >= geo.h for ib, _ in st.swaps)
 
 
 def _storage_bitperm(layout, d: int, to_basis: bool) -> list:
@@ -245,6 +259,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
     compiled = None
     norms = None
     events = []  # (kind, start, end)
+    ovl = {"pre": {}, "unpack": {}, "comm": None}  # overlapped remap events
     fused_order = []  # task ids of executed ApplyFused, in order
 
     def fail(exc):
@@ -296,7 +311,9 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 fail(PlanInvalid("compute before Alloc"))
             st = compiled.steps[task.id]
             slot = len(fused_order)
-            if st.count:
+            if st.count and compiled.overlap:
+                _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, stream, ovl)
+            elif st.count:
                 _run_descs(compiled, st.first, st.count, state, rows_eff, L, norms, grid_limit, stream)
             elif slot > 0:  # relabel-only leaf: the state (and its norm) is unchanged
                 norms[slot:slot + 1].copy_(norms[slot - 1:slot])
@@ -319,7 +336,12 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 fail(PlanInvalid("Exchange without matching Pack"))
             swaps = task.payload["swaps"]
             m = len(swaps)
-            launches = _remap(state, compiled.steps[task.id].swaps, geo, group, stream)
+            xst = compiled.steps[task.id]
+            if xst.pre in compiled.overlap and compiled.overlap[xst.pre] is xst:
+                launches, ce0, ce1 = _remap_overlapped(state, xst, geo, group, ovl)
+                events.append(("Exchange", ce0, ce1))
+            else:
+                launches = _remap(state, xst.swaps, geo, group, stream)
             stats.kernel_launches += launches
             moved = nranks * ((1 << m) - 1) * (1 << (L - m))
             messages = nranks * ((1 << m) - 1)
@@ -374,7 +396,96 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
     return RunResult(state=dstate, histogram=histogram, stats=stats)
 
 
-def _run_descs(compiled, first, count, state, rows_eff, L, norms, grid_limit, stream) -> None:
+OVERLAP_BITS = int(os.environ.get("SVB200_OVERLAP_BITS", "2"))
+OVERLAP_GRID = int(os.environ.get("SVB200_OVERLAP_GRID", "132"))  # leave SMs to NCCL / unpack
+
+
+def _part_values(cbits, c, fbits):
+    """Device-bit and tile-index encodings of chunk value c (cbits[0] = MSB)."""
+    k = len(cbits)
+    val = tid = 0
+    fpos = {b: i for i, b in enumerate(fbits)}
+    for j, b in enumerate(cbits):
+        if (c >> (k - 1 - j)) & 1:
+            val |= 1 << b
+            tid |= 1 << fpos[b]
+    return val, tid
+
+
+def _launch_part(compiled, di, state, norms, grid_limit, stream, cbits, c) -> None:
+    lib = _native.load()
+    d = compiled.descs[di]
+    K, D = int(d["K"]), int(d["D"])
+    tin = set(int(x) for x in d["tin"][:K])
+    fbits = [b for b in range(D) if b not in tin]
+    val, tid = _part_values(cbits, c, fbits)
+    ntiles = 1 << (D - K - len(cbits))
+    rc = lib.svb_jit_launch_sweep_part(compiled.kernels[di], state.buf.data_ptr(), compiled.blob.data_ptr(),
+                                       compiled.descs[di:di + 1].ctypes.data,
+                                       norms.data_ptr() if norms is not None else None,
+                                       grid_limit, val, tid, ntiles, stream)
+    _native.check(rc, "svb_jit_launch_sweep_part")
+
+
+def _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, stream, ovl) -> None:
+    """Sweeps of one ApplyFused task; the one before / after an overlapped remap
+    runs in parts linked by events to the remap's chunks on the comm stream."""
+    grid = min(grid_limit or prog_sms(), OVERLAP_GRID)
+    for di in range(st.first, st.first + st.count):
+        xst = compiled.overlap.get(di)
+        if xst is None:
+            _run_descs(compiled, di, 1, state, rows_eff, L, norms, grid_limit, stream)
+            continue
+        nparts = 1 << len(xst.cbits)
+        cur = torch.cuda.current_stream()
+        if di == xst.pre:
+            evs = []
+            for c in range(nparts):
+                _launch_part(compiled, di, state, norms, grid, stream, xst.cbits, c)
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                evs.append(ev)
+            ovl["pre"][id(xst)] = evs
+        else:  # post: each part waits for its chunk of the remap
+            evs = ovl["unpack"].pop(id(xst))
+            for c in range(nparts):
+                cur.wait_event(evs[c])
+                _launch_part(compiled, di, state, norms, grid, stream, xst.cbits, c)
+
+
+def prog_sms() -> int:
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
+def _remap_overlapped(state, xst, geo, group, ovl):
+    """Chunked remap on a side stream: chunk c starts when part c of the sweep
+    before has been written and releases part c of the sweep after."""
+    from . import comm
+
+    if ovl["comm"] is None:
+        ovl["comm"] = torch.cuda.Stream()
+    cs = ovl["comm"]
+    remote = [(ib - geo.h, lb) for ib, lb in xst.swaps]
+    pre_evs = ovl["pre"].pop(id(xst))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    outs = []
+    with torch.cuda.stream(cs):
+        cs.wait_event(pre_evs[0])
+        e0.record(cs)
+        for c, ev in enumerate(pre_evs):
+            cs.wait_event(ev)
+            launches += comm.exchange(state, remote, geo, group, cbits=xst.cbits, cval=c)
+            done = torch.cuda.Event()
+            done.record(cs)
+            outs.append(done)
+        e1.record(cs)
+    ovl["unpack"][id(xst)] = outs
+    return launches, e0, e1
+
+
+def _run_descs(compiled, first, count, state, rows_eff, L, norms, grid_limit, stream,
+               skip=()) -> None:
     lib = _native.load()
     if not count:
         return
@@ -386,6 +497,8 @@ def _run_descs(compiled, first, count, state, rows_eff, L, norms, grid_limit, st
         _native.check(rc, "svb_run_sweeps")
         return
     for i in range(count):
+        if first + i in skip:
+            continue
         rc = lib.svb_jit_launch_sweep(compiled.kernels[first + i], state.buf.data_ptr(),
                                       compiled.blob.data_ptr(), descs[i:i + 1].ctypes.data, nptr,
                                       grid_limit, stream)

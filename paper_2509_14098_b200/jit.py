@@ -116,7 +116,11 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     st_flip = int(desc["st_flip"])
     nct = int(desc["nctab"])
     fbits = [b for b in range(D) if b not in tin]
-    ntiles = 1 << (D - K)
+    # chunk bits: fixed per launch (runtime part_val) so a sweep can run in
+    # parts that overlap a remap; the tile index enumerates the other bits
+    cbits = [b for b in desc.get("cbits", ()) if b in fbits] if hasattr(desc, "get") else []
+    fprime = [b for b in fbits if b not in cbits]
+    fpos = {b: i for i, b in enumerate(fbits)}
     tb = K - rb  # thread bits
 
     L = []
@@ -125,7 +129,8 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     w(f"// prefetch={os.environ.get('SVB200_JIT_PREFETCH', 'early')}")
     w(f'extern "C" __global__ void __launch_bounds__({NT}, 1)')
     w(f"{name}(double2* __restrict__ state, const double2* __restrict__ tab, "
-      "const svb_cterm* __restrict__ cterms, const int* __restrict__ cofs, double* __restrict__ norm_out) {")
+      "const svb_cterm* __restrict__ cterms, const int* __restrict__ cofs, double* __restrict__ norm_out, "
+      "const u64 part_val, const u64 part_tid, const long long ntiles) {")
     w("  extern __shared__ __align__(16) double2 smem[];")
     w("  __shared__ double red[32];")
     w("  const int t = threadIdx.x;")
@@ -161,7 +166,13 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     w(f"  long long tile_id = blockIdx.x;")
 
     def origin(var):
-        return _deposit(var, fbits) if fbits else "0ull"
+        dep = _deposit(var, fprime) if fprime else "0ull"
+        return f"(({dep}) | part_val)" if cbits else dep
+
+    def full_tid(var):  # index over all fixed bits (per-tile slot LUTs)
+        if not cbits:
+            return var
+        return f"((long long)(({_deposit(var, [fpos[b] for b in fprime])}) | part_tid))"
 
     TILE = 1 << K
     nst = sum(1 for op in ops if int(op["kind"]) == prog.OP_STAGE)
@@ -220,19 +231,19 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     # prefetch of tile i+1 and the store of tile i-1 are issued in slices
     # between its stages, so loads, stores and FP64 work overlap.
     if not zero_init:
-        w(f"  if (tile_id < {ntiles}ll) {{")
+        w("  if (tile_id < ntiles) {")
         w(f"    const u64 b0 = {origin('tile_id')};")
         prefetch_items("smem", "b0", list(range(NR)))
         w("  }")
     w("  int iter = 0;")
-    w(f"  for (; tile_id < {ntiles}ll; ++iter, tile_id += gridDim.x) {{")
+    w("  for (; tile_id < ntiles; ++iter, tile_id += gridDim.x) {")
     w("    const int r3 = iter % 3;")
     w(f"    double2* const tile = smem + r3 * {TILE};")
     w(f"    double2* const nbuf = smem + (r3 == 2 ? 0 : r3 + 1) * {TILE};")
     w(f"    double2* const pbuf = smem + (r3 == 0 ? 2 : r3 - 1) * {TILE};")
     w(f"    const u64 base = {origin('tile_id')};")
     w(f"    double2* const ctab = ctab_base + (iter & 1) * {max(nct, 1)};")
-    w(f"    const bool has_next = tile_id + gridDim.x < {ntiles}ll;")
+    w("    const bool has_next = tile_id + gridDim.x < ntiles;")
     w("    const long long nx = tile_id + gridDim.x;")
     w(f"    const u64 bn = {origin('nx')};")
     w("    const long long px = tile_id - gridDim.x;")
@@ -240,11 +251,12 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     if nct:
         lut_off, nch = int(desc["lut_off"]), int(desc["lut_nch"])
         residual = desc["residual"]
+        w(f"    const long long ftid = {full_tid('tile_id')};")
         w(f"    for (int i = t; i < {nct}; i += {NT}) {{")
         w(f"      const double2* lt = tab + {lut_off} + i * {nch * 256};")
-        w("      double2 acc = __ldg(lt + (tile_id & 255));")
+        w("      double2 acc = __ldg(lt + (ftid & 255));")
         for c in range(1, nch):
-            w(f"      acc = cmul(acc, __ldg(lt + {c * 256} + ((tile_id >> {8 * c}) & 255)));")
+            w(f"      acc = cmul(acc, __ldg(lt + {c * 256} + ((ftid >> {8 * c}) & 255)));")
         if any(residual):
             for s_, terms in enumerate(residual):
                 if not terms:

@@ -537,6 +537,11 @@ class Step:
     first: int = 0  # first descriptor
     count: int = 0  # descriptors
     swaps: list = field(default_factory=list)  # exchange: (rank int bit, physical local bit)
+    # exchange overlap: chunk bits (physical) shared by the sweep before and the
+    # sweep after, so both can run in 2^len(cbits) parts pipelined with the remap
+    cbits: list = field(default_factory=list)
+    pre: int = -1  # descriptor of the sweep before the remap
+    post: int = -1  # descriptor of the sweep after the remap
 
 
 @dataclass
@@ -626,8 +631,44 @@ def _pad_displaced(tile: set, where: list, look: _Lookahead, K: int, L: int) -> 
             tile |= add
 
 
+def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int) -> None:
+    """Chunk bits for remaps whose neighbouring sweeps can run in parts."""
+    if nbits <= 0:
+        return
+    L = geo.L
+    for i, st in enumerate(steps):
+        if st.kind != "exchange" or not st.swaps:
+            continue
+        # nearest sweeps on each side; relabel-only leaves (count 0) move no data
+        prev = nxt = None
+        for x in reversed(steps[:i]):
+            if x.kind == "exchange":
+                break
+            if x.count:
+                prev = x
+                break
+        for x in steps[i + 1:]:
+            if x.kind == "exchange":
+                break
+            if x.count:
+                nxt = x
+                break
+        if prev is None or nxt is None:
+            continue
+        pre, post = prev.first + prev.count - 1, nxt.first
+        busy = set(buf.descs[pre]["tin"]) | set(buf.descs[post]["tin"]) | {lb for _, lb in st.swaps}
+        cand = [b for b in range(L - 1, -1, -1) if b not in busy]
+        if not cand:
+            continue
+        cb = sorted(cand[:nbits])
+        st.cbits, st.pre, st.post = cb, pre, post
+        buf.descs[pre]["cbits"] = cb
+        buf.descs[post]["cbits"] = cb
+
+
 def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_BITS,
-                max_materialize: int = 64, rb: int = RB, fuse: bool = True) -> DeviceProgram:
+                max_materialize: int = 64, rb: int = RB, fuse: bool = True,
+                overlap_bits: int = 0) -> DeviceProgram:
     """Compile every ApplyFused task of a plan for one device, with a global layout.
 
     The physical layout is a permutation `where` of the local bits that the
@@ -747,6 +788,8 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
                 break
         steps.append(Step("sweeps", task.id, first, len(buf.descs) - first))
         slot += 1
+
+    _plan_overlap(steps, buf, geo, overlap_bits)
 
     # restore the reference layout
     first = len(buf.descs)
