@@ -152,12 +152,13 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
     steps = {}
     for st in dp.steps:
         steps[st.task_id] = st
-    # sweeps launched in parts around an overlapped remap
-    overlap = {}  # descriptor -> exchange step
+    # sweeps launched in parts around an overlapped remap: descriptor ->
+    # {"pre": exchange it feeds, "post": exchange it waits for}
+    overlap = {}
     for st in dp.steps:
         if st.kind == "exchange" and st.cbits and all(ib >= geo.h for ib, _ in st.swaps):
-            overlap[st.pre] = st
-            overlap[st.post] = st
+            overlap.setdefault(st.pre, {})["pre"] = st
+            overlap.setdefault(st.post, {})["post"] = st
     out = _Compiled(dev_blob, descs, steps, dp.init_perm, dp.n_fused, time.perf_counter() - t0,
                     host, n_sweeps=len(dp.buf.descs))
     out.overlap = overlap if use_jit else {}
@@ -337,7 +338,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             swaps = task.payload["swaps"]
             m = len(swaps)
             xst = compiled.steps[task.id]
-            if xst.pre in compiled.overlap and compiled.overlap[xst.pre] is xst:
+            if compiled.overlap.get(xst.pre, {}).get("pre") is xst:
                 launches, ce0, ce1 = _remap_overlapped(state, xst, geo, group, ovl)
                 events.append(("Exchange", ce0, ce1))
             else:
@@ -432,25 +433,26 @@ def _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, s
     runs in parts linked by events to the remap's chunks on the comm stream."""
     grid = min(grid_limit or prog_sms(), OVERLAP_GRID)
     for di in range(st.first, st.first + st.count):
-        xst = compiled.overlap.get(di)
-        if xst is None:
+        roles = compiled.overlap.get(di)
+        if not roles:
             _run_descs(compiled, di, 1, state, rows_eff, L, norms, grid_limit, stream)
             continue
-        nparts = 1 << len(xst.cbits)
+        feeds, waits = roles.get("pre"), roles.get("post")
+        cbits = (feeds or waits).cbits  # the planner gives both roles the same chunk bits
+        nparts = 1 << len(cbits)
         cur = torch.cuda.current_stream()
-        if di == xst.pre:
-            evs = []
-            for c in range(nparts):
-                _launch_part(compiled, di, state, norms, grid, stream, xst.cbits, c)
+        wait_evs = ovl["unpack"].pop(id(waits)) if waits is not None else None
+        evs = []
+        for c in range(nparts):
+            if wait_evs is not None:  # part c needs chunk c of the previous remap
+                cur.wait_event(wait_evs[c])
+            _launch_part(compiled, di, state, norms, grid, stream, cbits, c)
+            if feeds is not None:
                 ev = torch.cuda.Event()
                 ev.record(cur)
                 evs.append(ev)
-            ovl["pre"][id(xst)] = evs
-        else:  # post: each part waits for its chunk of the remap
-            evs = ovl["unpack"].pop(id(xst))
-            for c in range(nparts):
-                cur.wait_event(evs[c])
-                _launch_part(compiled, di, state, norms, grid, stream, xst.cbits, c)
+        if feeds is not None:
+            ovl["pre"][id(feeds)] = evs
 
 
 def prog_sms() -> int:

@@ -657,10 +657,16 @@ def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int) -> None:
             continue
         pre, post = prev.first + prev.count - 1, nxt.first
         busy = set(buf.descs[pre]["tin"]) | set(buf.descs[post]["tin"]) | {lb for _, lb in st.swaps}
-        cand = [b for b in range(L - 1, -1, -1) if b not in busy]
-        if not cand:
-            continue
-        cb = sorted(cand[:nbits])
+        have = buf.descs[pre].get("cbits")  # pre is also the post of an earlier remap
+        if have:
+            if busy & set(have) or buf.descs[post].get("cbits"):
+                continue
+            cb = list(have)
+        else:
+            cand = [b for b in range(L - 1, -1, -1) if b not in busy]
+            if not cand or buf.descs[post].get("cbits"):
+                continue
+            cb = sorted(cand[:nbits])
         st.cbits, st.pre, st.post = cb, pre, post
         buf.descs[pre]["cbits"] = cb
         buf.descs[post]["cbits"] = cb
