@@ -397,7 +397,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
     return RunResult(state=dstate, histogram=histogram, stats=stats)
 
 
-OVERLAP_BITS = int(os.environ.get("SVB200_OVERLAP_BITS", "2"))
+OVERLAP_BITS = int(os.environ.get("SVB200_OVERLAP_BITS", "0"))  # NCCL overlap measured slower (SM contention)
 OVERLAP_GRID = int(os.environ.get("SVB200_OVERLAP_GRID", "132"))  # leave SMs to NCCL / unpack
 
 
