@@ -120,6 +120,7 @@ class _Compiled:
     compile_seconds: float
     host_blob: np.ndarray = field(repr=False, default=None)
     overlap: dict = field(default_factory=dict)  # descriptor -> overlapped exchange step
+    cbits: dict = field(default_factory=dict)  # descriptor -> chunk bits its kernel was built with
     kernels: list | None = None  # per-descriptor JIT kernel handles (None: interpreter)
     jit_seconds: float = 0.0
     zero_init: dict = field(default_factory=dict)  # descriptors that synthesise |0...0>
@@ -162,6 +163,7 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
     out = _Compiled(dev_blob, descs, steps, dp.init_perm, dp.n_fused, time.perf_counter() - t0,
                     host, n_sweeps=len(dp.buf.descs))
     out.overlap = overlap if use_jit else {}
+    out.cbits = {i: d["cbits"] for i, d in enumerate(dp.buf.descs) if d.get("cbits")} if use_jit else {}
     if use_jit and dp.buf.descs:
         from . import jit as jitmod
 
@@ -500,6 +502,11 @@ def _run_descs(compiled, first, count, state, rows_eff, L, norms, grid_limit, st
         return
     for i in range(count):
         if first + i in skip:
+            continue
+        cb = compiled.cbits.get(first + i)
+        if cb:  # a kernel compiled for part launches: run all parts in order
+            for c in range(1 << len(cb)):
+                _launch_part(compiled, first + i, state, norms, grid_limit, stream, cb, c)
             continue
         rc = lib.svb_jit_launch_sweep(compiled.kernels[first + i], state.buf.data_ptr(),
                                       compiled.blob.data_ptr(), descs[i:i + 1].ctypes.data, nptr,

@@ -639,6 +639,8 @@ def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int) -> None:
     for i, st in enumerate(steps):
         if st.kind != "exchange" or not st.swaps:
             continue
+        if any(ib < geo.h for ib, _ in st.swaps):
+            continue  # part of the remap is an in-HBM bit swap over all chunks
         # nearest sweeps on each side; relabel-only leaves (count 0) move no data
         prev = nxt = None
         for x in reversed(steps[:i]):

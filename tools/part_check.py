@@ -18,6 +18,11 @@ def main(names):
     for name in names:
         plan = planmod.load(str(ROOT / "plans" / f"{name}.json.gz"))
         geo = prog.DeviceGeometry(d=plan.d, g=plan.g, h=plan.g, rank_base=0, pad_to=4)
+        ref = prog.plan_device(plan, geo, rb=4)  # same sweeps, no chunk bits
+        rblob, rdescs, _ = prog.pack(ref.buf)
+        drblob = torch.from_numpy(rblob).cuda()
+        rnames, rcubins = jit.build_kernels(ref.buf)
+        rkern = [jit.load_kernel(n, c, 0) for n, c in zip(rnames, rcubins)]
         dp = prog.plan_device(plan, geo, rb=4)
         L = geo.L
         for d in dp.buf.descs:  # chunk bits: the two highest local bits outside the tile
@@ -48,8 +53,8 @@ def main(names):
 
             sa = S()
             sa.buf = a
-            _native.check(lib.svb_jit_launch_sweep(comp.kernels[i], a.data_ptr(), dblob.data_ptr(),
-                                                   descs[i:i + 1].ctypes.data, None, 0, st), "whole")
+            _native.check(lib.svb_jit_launch_sweep(rkern[i], a.data_ptr(), drblob.data_ptr(),
+                                                   rdescs[i:i + 1].ctypes.data, None, 0, st), "whole")
             sb = S()
             sb.buf = b
             for c in range(1 << len(cb)):
