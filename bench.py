@@ -177,8 +177,12 @@ def run_reference_arm(args) -> None:
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": CPU_SAMPLE_PLAN, "qubits": plan.d, "hierarchy": [plan.d, 12],
-                   "note": "CPU sample of the QFT/[d,12] workload family; reference is single-threaded"},
+        "config": {"workload": workload_name(args.workload, max(args.gpus, 1))[0],
+                   "sample": f"{CPU_SAMPLE_PLAN}: the same QFT family and [d, 12] hierarchy at "
+                             f"{plan.d} qubits (the full workload takes ~70 min per run on one core); "
+                             "value = algorithmic bytes / time, size-normalised like the GPU arm",
+                   "note": "reference run_plan semantics with the reference's compiled _core.pyx "
+                           "kernels; single-threaded like the reference"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": kind,
                          "sample": f"{CPU_SAMPLE_PLAN} full plan per step, host cores {os.cpu_count()}"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
