@@ -204,6 +204,51 @@ int svb_jit_launch_sweep_part(void* kernel, svb_c128* state, const void* prog,
                               uint64_t part_val, uint64_t part_tid, int64_t ntiles,
                               void* stream);
 
+/* ------------------------------------------------------------------------
+ * 6. Peer-memory remap (paper_2509_14098_b200/comm.py), replacing the
+ *    inter-GPU Pack -> Exchange -> Unpack of svpart/executor.py:224-281.
+ *
+ * svb_dev_alloc / svb_dev_free: plain cudaMalloc'd state storage that can
+ *   be shared with the other processes of the job.
+ * svb_ipc_handle: the 64-byte CUDA IPC handle of an svb_dev_alloc pointer;
+ *   svb_ipc_open maps a peer's handle into this process (svb_ipc_close).
+ * svb_peer_swap: in-place pairwise swap with npeers peers.  The m local
+ *   bits lbits[0..m) select regions; for peer j, pairs
+ *   k in [first[j], first[j]+count[j]) of local region sel_local[j] and the
+ *   peer's region sel_remote[j] (selector bit m-1-i <-> lbits[i]) are
+ *   exchanged.  k enumerates rows (outer) then the free local bits in
+ *   ascending order, like svb_pack_region.  The two processes of a pair
+ *   must split the k range between them and order the launch between
+ *   cross-process barriers.  grid_limit caps the CTAs per peer (0: fill the
+ *   GPU), block is the CTA size (0: 256); a small grid of 1024-thread CTAs
+ *   leaves the other SMs to sweeps running concurrently.
+ * ---------------------------------------------------------------------- */
+int svb_dev_alloc(size_t bytes, void** ptr);
+int svb_dev_free(void* ptr);
+int svb_ipc_handle(void* ptr, void* handle64);
+int svb_ipc_open(const void* handle64, void** ptr);
+int svb_ipc_close(void* ptr);
+/* svb_peer_swap_bulk: the same swap driven by the bulk-copy (TMA) engine:
+ *   `grid` persistent CTAs of one warp, each a ring of `stages` shared-memory
+ *   stages of 2 x piece_bytes (power of two), `ahead` of them loading
+ *   (0: stages - 2) while the rest store; leaves the other SMs' compute
+ *   free, so a remap can run beside the sweeps. */
+int svb_peer_swap_bulk(svb_c128* local, void* const* peers, int npeers, int64_t rows, int L,
+                       const int32_t* lbits, int m, const uint64_t* sel_local,
+                       const uint64_t* sel_remote, const int64_t* first, const int64_t* count,
+                       int grid, int piece_bytes, int stages, int ahead, void* stream);
+/* Stream-ordered 32-bit flags (cuStreamWriteValue32 / cuStreamWaitValue32):
+ *   write `value` to addr (own or a mapped peer's device memory) after all
+ *   earlier work of the stream; or hold the stream until *addr >= value. */
+int svb_stream_write_u32(void* addr, uint32_t value, void* stream);
+int svb_stream_wait_u32(void* addr, uint32_t value, void* stream);
+/* svb_copy: n-amplitude SM copy; either pointer may be a mapped peer's. */
+int svb_copy(svb_c128* dst, const svb_c128* src, int64_t n, int grid_limit, void* stream);
+int svb_peer_swap(svb_c128* local, void* const* peers, int npeers, int64_t rows, int L,
+                  const int32_t* lbits, int m, const uint64_t* sel_local,
+                  const uint64_t* sel_remote, const int64_t* first, const int64_t* count,
+                  int grid_limit, int block, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

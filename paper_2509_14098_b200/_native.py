@@ -46,6 +46,18 @@ _SIGS = {
     "svb_jit_launch_sweep": ([_vp, _vp, _vp, _vp, _vp, _int, _vp], _int),
     "svb_jit_launch_sweep_part": ([_vp, _vp, _vp, _vp, _vp, _int, _c.c_uint64, _c.c_uint64, _i64, _vp],
                                   _int),
+    "svb_dev_alloc": ([_sz, _c.POINTER(_vp)], _int),
+    "svb_dev_free": ([_vp], _int),
+    "svb_ipc_handle": ([_vp, _vp], _int),
+    "svb_ipc_open": ([_vp, _c.POINTER(_vp)], _int),
+    "svb_ipc_close": ([_vp], _int),
+    "svb_peer_swap_bulk": ([_vp, _vp, _int, _i64, _int, _pi32, _int, _vp, _vp, _vp, _vp, _int, _int, _int, _int,
+                            _vp],
+                           _int),
+    "svb_stream_write_u32": ([_vp, _u32, _vp], _int),
+    "svb_stream_wait_u32": ([_vp, _u32, _vp], _int),
+    "svb_copy": ([_vp, _vp, _i64, _int, _vp], _int),
+    "svb_peer_swap": ([_vp, _vp, _int, _i64, _int, _pi32, _int, _vp, _vp, _vp, _vp, _int, _int, _vp], _int),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -164,3 +164,234 @@ def exchange(state, remote: list, geo, group, mover=None, chunk_elems: int | Non
                 launches += 1
         pending = nxt
     return launches
+
+
+# ---------------------------------------------------------------------------
+# Peer-memory remap (default on CUDA): symmetric state storage mapped into
+# every process with CUDA IPC, one in-place bulk-copy swap kernel per
+# exchange (or per chunk of it), ordered between GPUs by flag words that the
+# streams write into each other's memory.
+# ---------------------------------------------------------------------------
+
+PEER_MODE = os.environ.get("SVB200_REMAP", "peer")  # "peer" | "nccl"
+# bulk swap geometry: 148 one-warp CTAs with 3 x 2 x 4 KiB stages (24.7 KB of
+# shared memory, 48 registers) fit on every SM beside a running sweep CTA and
+# still reach ~690 GB/s per direction (tools/p2p_bench.py, round 1)
+SWAP_GRID = int(os.environ.get("SVB200_SWAP_GRID", "148"))
+SWAP_PIECE = int(os.environ.get("SVB200_SWAP_PIECE", "4096"))
+SWAP_STAGES = int(os.environ.get("SVB200_SWAP_STAGES", "3"))
+SWAP_AHEAD = int(os.environ.get("SVB200_SWAP_AHEAD", "1"))
+
+FLAG_RANKS = 64  # flag words: [kind][source rank][chunk], uint32 epochs
+FLAG_CHUNKS = 64
+FLAG_BYTES = 2 * FLAG_RANKS * FLAG_CHUNKS * 4
+READY, DONE = 0, 1
+
+
+class _Arena:
+    """One cudaMalloc'd state buffer (+ flag words) of this process, reusable across runs."""
+
+    def __init__(self, lib, device, nbytes: int):
+        import ctypes
+
+        from . import _native
+
+        ptr = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _native.check(lib.svb_dev_alloc(nbytes + FLAG_BYTES, ctypes.byref(ptr)), "svb_dev_alloc")
+            h = (ctypes.c_uint8 * 64)()
+            _native.check(lib.svb_ipc_handle(ptr, h), "svb_ipc_handle")
+            flags = torch.as_tensor(_Lease(self, FLAG_BYTES // 4, ptr.value + nbytes, "<i4", hold=False),
+                                    device=torch.device("cuda", device))
+            flags.zero_()
+        self.ptr, self.nbytes, self.device = ptr.value, nbytes, device
+        self.handle = bytes(h)
+        self.busy = False
+        self.epoch = 0  # last flag value used with this buffer
+
+
+class _Lease:
+    """Keeps an arena busy while any tensor viewing it is alive."""
+
+    def __init__(self, arena: _Arena, n: int, ptr: int | None = None, typestr: str = "<c16",
+                 hold: bool = True):
+        self.arena = arena if hold else None
+        if hold:
+            arena.busy = True
+        self.__cuda_array_interface__ = {
+            "shape": (n,), "typestr": typestr, "data": (arena.ptr if ptr is None else ptr, False),
+            "version": 2, "strides": None,
+        }
+
+    def __del__(self):
+        if self.arena is not None:
+            self.arena.busy = False
+
+
+class PeerContext:
+    """This process's view of the symmetric state: the peers' mapped state
+    and flag pointers and the flag epoch the group agreed on."""
+
+    def __init__(self, me: int, arena: _Arena, peers: dict, peer_flags: dict, epoch: int):
+        self.me = me
+        self.arena = arena
+        self.peers = peers
+        self.peer_flags = peer_flags
+        self.flags = arena.ptr + arena.nbytes
+        self.epoch = epoch
+
+    def next_epoch(self) -> int:
+        self.epoch += 1
+        self.arena.epoch = self.epoch
+        return self.epoch
+
+    @staticmethod
+    def _off(kind: int, src: int, chunk: int) -> int:
+        return 4 * ((kind * FLAG_RANKS + src) * FLAG_CHUNKS + chunk)
+
+    def signal(self, kind, chunk, ranks, epoch, stream) -> None:
+        """After the stream's earlier work, tell `ranks` that this process reached (kind, chunk)."""
+        from . import _native
+
+        lib = _native.load()
+        for r in ranks:
+            _native.check(lib.svb_stream_write_u32(self.peer_flags[r] + self._off(kind, self.me, chunk),
+                                                   epoch, stream), "svb_stream_write_u32")
+
+    def wait(self, kind, chunk, ranks, epoch, stream) -> None:
+        """Hold the stream until every rank in `ranks` signalled (kind, chunk) for this epoch."""
+        from . import _native
+
+        lib = _native.load()
+        for r in ranks:
+            _native.check(lib.svb_stream_wait_u32(self.flags + self._off(kind, r, chunk), epoch, stream),
+                          "svb_stream_wait_u32")
+
+
+_ARENAS: dict = {}  # device index -> [_Arena]
+_PEER_PTRS: dict = {}  # (device index, peer handle bytes) -> mapped pointer
+
+
+def symmetric_buffer(n: int, device, group):
+    """A complex128 buffer of n amplitudes on `device` in storage every
+    process of `group` has mapped; returns (tensor, PeerContext).
+
+    Collective: every process of the group calls it with the same n.  A
+    buffer goes back to the pool when the last tensor viewing it dies.
+    """
+    import ctypes
+
+    import torch.distributed as dist
+
+    from . import _native
+
+    lib = _native.load()
+    device = torch.device(device)
+    di = device.index if device.index is not None else torch.cuda.current_device()
+    nbytes = n * 16
+    pool = _ARENAS.setdefault(di, [])
+    arena = next((a for a in pool if not a.busy and a.nbytes == nbytes), None)
+    if arena is None:
+        arena = _Arena(lib, di, nbytes)
+        pool.append(arena)
+    buf = torch.as_tensor(_Lease(arena, n), device=device)
+    me, world = dist.get_rank(group), dist.get_world_size(group)
+    rec = np.frombuffer(arena.handle + int(arena.epoch).to_bytes(8, "little"), dtype=np.uint8)
+    mine = torch.from_numpy(rec.copy()).to(device)
+    allr = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(allr, mine, group=group)
+    peers, peer_flags, epoch = {}, {}, 0
+    for r, t in enumerate(allr):
+        raw_all = bytes(t.cpu().numpy().tobytes())
+        epoch = max(epoch, int.from_bytes(raw_all[64:], "little"))
+        if r == me:
+            continue
+        hb = raw_all[:64]
+        key = (di, hb)
+        if key not in _PEER_PTRS:
+            ptr = ctypes.c_void_p()
+            raw = (ctypes.c_uint8 * 64).from_buffer_copy(hb)
+            with torch.cuda.device(di):
+                _native.check(lib.svb_ipc_open(raw, ctypes.byref(ptr)), "svb_ipc_open")
+            _PEER_PTRS[key] = ptr.value
+        peers[r] = _PEER_PTRS[key]
+        peer_flags[r] = peers[r] + nbytes
+    return buf, PeerContext(me, arena, peers, peer_flags, epoch)
+
+
+def swap_args(state, remote: list, me: int, ctx: PeerContext, cbits=None, cval: int = 0):
+    """Arguments of svb_peer_swap(_bulk) for one exchange (or its chunk cval
+    over `cbits`): process w and peer p = w[e := v] own the pairs
+    w.region(v)[k] <-> p.region(alpha_w)[k]; the lower-ranked of the two swaps
+    the first half of k, the other the second half."""
+    import ctypes
+
+    m = len(remote)
+    ebits = [e for e, _ in remote]
+    cbits = list(cbits or [])
+    k = len(cbits)
+    lbits = [lb for _, lb in remote] + cbits
+    alpha = 0
+    for e in ebits:
+        alpha = (alpha << 1) | ((me >> e) & 1)
+    # partners in order of sel ^ alpha: round s pairs every process with a
+    # distinct partner (a perfect matching), so no process is every partner's first
+    plans = sorted(peer_plan(me, ebits, m), key=lambda pp: pp.sel ^ alpha)
+    mm = m + k
+    region = state.rows << (state.L - mm)
+    half = region // 2
+    n = len(plans)
+    keep = [np.asarray(lbits, dtype=np.int32),
+            np.asarray([(pp.sel << k) | cval for pp in plans], dtype=np.uint64),
+            np.full(n, (alpha << k) | cval, dtype=np.uint64),
+            np.asarray([0 if me < pp.peer else half for pp in plans], dtype=np.int64),
+            np.asarray([half if me < pp.peer else region - half for pp in plans], dtype=np.int64)]
+    ptrs = (ctypes.c_void_p * n)(*[ctx.peers[pp.peer] for pp in plans])
+    from . import _native
+
+    args = (state.buf.data_ptr(), ptrs, n, state.rows, state.L, keep[0].ctypes.data_as(_native._pi32), mm,
+            keep[1].ctypes.data, keep[2].ctypes.data, keep[3].ctypes.data, keep[4].ctypes.data)
+    return args, [pp.peer for pp in plans], (keep, ptrs)
+
+
+def peer_exchange(state, remote: list, ctx: PeerContext, stream, epoch: int, cbits=None, cval: int = 0,
+                  wait_done: bool = True) -> int:
+    """One exchange (or chunk `cval` of it) as a flag-ordered bulk swap on
+    `stream`: signal READY, wait for every partner's READY, swap, signal
+    DONE and (wait_done) wait for every partner's DONE -- without it the
+    caller must wait_partners_done() before touching the chunk again.
+    Returns the kernel launches."""
+    from . import _native
+
+    lib = _native.load()
+    from .executor import _mark
+
+    args, partners, _keep = swap_args(state, remote, ctx.me, ctx, cbits, cval)
+    ts = None
+    if _TRACE_ON():
+        cur = torch.cuda.current_stream()
+        ts = cur if cur.cuda_stream == stream else torch.cuda.ExternalStream(stream)
+    _mark(f"x{epoch}.{cval} ready-signal", ts)
+    ctx.signal(READY, cval, partners, epoch, stream)
+    ctx.wait(READY, cval, partners, epoch, stream)
+    _mark(f"x{epoch}.{cval} swap start", ts)
+    _native.check(lib.svb_peer_swap_bulk(*args, SWAP_GRID, SWAP_PIECE, SWAP_STAGES, SWAP_AHEAD, stream),
+                  "svb_peer_swap_bulk")
+    _mark(f"x{epoch}.{cval} swap end", ts)
+    ctx.signal(DONE, cval, partners, epoch, stream)
+    if wait_done:
+        ctx.wait(DONE, cval, partners, epoch, stream)
+        _mark(f"x{epoch}.{cval} done", ts)
+    return 1
+
+
+def wait_partners_done(state, remote: list, ctx: PeerContext, stream, epoch: int, cval: int = 0) -> None:
+    """Hold `stream` until every partner of this exchange finished its swap of chunk cval."""
+    partners = [pp.peer for pp in peer_plan(ctx.me, [e for e, _ in remote], len(remote))]
+    ctx.wait(DONE, cval, partners, epoch, stream)
+
+
+def _TRACE_ON() -> bool:
+    from . import executor
+
+    return executor._TRACE

@@ -112,6 +112,11 @@ extern "C" int svb_jit_load(const void* image, const char* kernel_name, void** k
   e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
                            cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(jit)");
+  // keep every SM at the full shared-memory carveout so a remap kernel can
+  // share the SM with a running sweep (csrc/peer.cu)
+  e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
+                           cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(jit carveout)");
   *kernel = reinterpret_cast<void*>(k);
   return SVB_OK;
 }

@@ -58,6 +58,7 @@ class RunStats:
     sweeps: int = 0
     kernel_launches: int = 0
     layout_seconds: float = 0.0  # trailing sweeps restoring the reference layout
+    trace: list = field(default_factory=list)  # (label, ms from run start) with SVB200_TRACE=1
 
 
 @dataclass
@@ -146,7 +147,7 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
     t0 = time.perf_counter()
     dist_run = _dist_info()[1] > 1
     dp = prog.plan_device(plan, geo, rb=JIT_REG_BITS if use_jit else prog.RB,
-                          overlap_bits=OVERLAP_BITS if (use_jit and dist_run) else 0)
+                          overlap_bits=_overlap_bits() if (use_jit and dist_run) else 0)
     blob, descs, _ = prog.pack(dp.buf)
     host = np.ascontiguousarray(blob)
     dev_blob = torch.from_numpy(host).to(device)
@@ -215,11 +216,19 @@ def _bitperm(src: torch.Tensor, dst: torch.Tensor, perm: list) -> None:
 class _State:
     """Device storage with a phantom pad so tiny states still fill 16 amplitudes."""
 
-    def __init__(self, rows: int, L: int, device, zero: bool = True):
+    def __init__(self, rows: int, L: int, device, zero: bool = True, group=None, peer: bool = False):
         self.rows, self.L = rows, L
         n = rows << L
-        alloc = torch.zeros if zero else torch.empty
-        self.buf = alloc(max(n, prog.NREG), dtype=torch.complex128, device=device)
+        self.ctx = None  # comm.PeerContext of the peer-memory remap
+        if peer:
+            from . import comm
+
+            self.buf, self.ctx = comm.symmetric_buffer(max(n, prog.NREG), device, group)
+            if zero:
+                self.buf.zero_()
+        else:
+            alloc = torch.zeros if zero else torch.empty
+            self.buf = alloc(max(n, prog.NREG), dtype=torch.complex128, device=device)
         self.blocks = self.buf[:n].view(rows, 1 << L)
 
 
@@ -262,7 +271,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
     compiled = None
     norms = None
     events = []  # (kind, start, end)
-    ovl = {"pre": {}, "unpack": {}, "comm": None}  # overlapped remap events
+    ovl = {"pre": {}, "unpack": {}, "comm": None, "peer": {}}  # overlapped remap events / flags
     fused_order = []  # task ids of executed ApplyFused, in order
 
     def fail(exc):
@@ -300,7 +309,10 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             compiled = compile_plan(plan, geo_eff, device, jit, zero_start=initial is None)
             stats.compile_seconds = compiled.compile_seconds + compiled.jit_seconds
             # when the first sweep synthesises |0...0> the state needs no memset
-            state = _State(rows, L, device, zero=not compiled.zero_init)
+            from . import comm
+
+            state = _State(rows, L, device, zero=not compiled.zero_init, group=group,
+                           peer=world > 1 and comm.PEER_MODE == "peer")
             if initial is None:
                 if rank_base == 0 and not compiled.zero_init:
                     state.blocks[0, 0] = 1.0  # |0...0> sits at index 0 in every layout
@@ -317,7 +329,9 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             if st.count and compiled.overlap:
                 _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, stream, ovl)
             elif st.count:
+                _mark(f"sweeps{st.first}-{st.first + st.count - 1} start")
                 _run_descs(compiled, st.first, st.count, state, rows_eff, L, norms, grid_limit, stream)
+                _mark(f"sweeps{st.first}-{st.first + st.count - 1} end")
             elif slot > 0:  # relabel-only leaf: the state (and its norm) is unchanged
                 norms[slot:slot + 1].copy_(norms[slot - 1:slot])
             elif initial is None:  # |0...0> (possibly not materialised yet) has norm 1
@@ -344,7 +358,9 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 launches, ce0, ce1 = _remap_overlapped(state, xst, geo, group, ovl)
                 events.append(("Exchange", ce0, ce1))
             else:
+                _mark(f"remap{task.id} start")
                 launches = _remap(state, xst.swaps, geo, group, stream)
+                _mark(f"remap{task.id} end")
             stats.kernel_launches += launches
             moved = nranks * ((1 << m) - 1) * (1 << (L - m))
             messages = nranks * ((1 << m) - 1)
@@ -378,6 +394,10 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
         stats.sweeps += mat.count
         stats.kernel_launches += mat.count
     torch.cuda.synchronize(device)
+    if _TRACE and _marks:
+        t0 = _marks[0][1]
+        stats.trace = [(lab, t0.elapsed_time(ev)) for lab, ev in _marks]
+        _marks.clear()
     for kind, e0, e1 in events:
         sec = e0.elapsed_time(e1) / 1e3
         if kind in ("Pack", "Exchange", "Unpack"):
@@ -399,8 +419,31 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
     return RunResult(state=dstate, histogram=histogram, stats=stats)
 
 
-OVERLAP_BITS = int(os.environ.get("SVB200_OVERLAP_BITS", "0"))  # NCCL overlap measured slower (SM contention)
-OVERLAP_GRID = int(os.environ.get("SVB200_OVERLAP_GRID", "132"))  # leave SMs to NCCL / unpack
+_TRACE = os.environ.get("SVB200_TRACE") == "1"
+_marks: list = []
+
+
+def _mark(label: str, stream=None) -> None:
+    """Record a timing event on `stream` (tracing only)."""
+    if _TRACE:
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        _marks.append((label, ev))
+
+
+def _overlap_bits() -> int:
+    """Chunk bits of remaps that overlap the sweeps around them.  On with the
+    peer-memory remap (its bulk-copy swap shares the SMs with the sweeps);
+    off with NCCL, whose kernels starve the persistent sweeps (round 1)."""
+    from . import comm
+
+    env = os.environ.get("SVB200_OVERLAP_BITS")
+    if env is not None:
+        return int(env)
+    return 3 if comm.PEER_MODE == "peer" else 0
+
+
+OVERLAP_GRID = int(os.environ.get("SVB200_OVERLAP_GRID", "0"))  # 0: every SM
 
 
 def _part_values(cbits, c, fbits):
@@ -433,11 +476,15 @@ def _launch_part(compiled, di, state, norms, grid_limit, stream, cbits, c) -> No
 def _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, stream, ovl) -> None:
     """Sweeps of one ApplyFused task; the one before / after an overlapped remap
     runs in parts linked by events to the remap's chunks on the comm stream."""
-    grid = min(grid_limit or prog_sms(), OVERLAP_GRID)
+    from . import comm
+
+    grid = min(grid_limit or prog_sms(), OVERLAP_GRID or prog_sms())
     for di in range(st.first, st.first + st.count):
         roles = compiled.overlap.get(di)
         if not roles:
+            _mark(f"sweep{di} start")
             _run_descs(compiled, di, 1, state, rows_eff, L, norms, grid_limit, stream)
+            _mark(f"sweep{di} end")
             continue
         feeds, waits = roles.get("pre"), roles.get("post")
         cbits = (feeds or waits).cbits  # the planner gives both roles the same chunk bits
@@ -448,7 +495,12 @@ def _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, s
         for c in range(nparts):
             if wait_evs is not None:  # part c needs chunk c of the previous remap
                 cur.wait_event(wait_evs[c])
+                if state.ctx is not None:  # ... swapped on both sides of every pair
+                    remote, epoch = ovl["peer"].pop((id(waits), c))
+                    comm.wait_partners_done(state, remote, state.ctx, cur.cuda_stream, epoch, c)
+            _mark(f"sweep{di}.part{c} start", cur)
             _launch_part(compiled, di, state, norms, grid, stream, cbits, c)
+            _mark(f"sweep{di}.part{c} end", cur)
             if feeds is not None:
                 ev = torch.cuda.Event()
                 ev.record(cur)
@@ -474,12 +526,18 @@ def _remap_overlapped(state, xst, geo, group, ovl):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
     outs = []
+    epoch = state.ctx.next_epoch() if state.ctx is not None else 0
     with torch.cuda.stream(cs):
         cs.wait_event(pre_evs[0])
         e0.record(cs)
         for c, ev in enumerate(pre_evs):
             cs.wait_event(ev)
-            launches += comm.exchange(state, remote, geo, group, cbits=xst.cbits, cval=c)
+            if state.ctx is not None:
+                launches += comm.peer_exchange(state, remote, state.ctx, cs.cuda_stream, epoch,
+                                               cbits=xst.cbits, cval=c, wait_done=False)
+                ovl["peer"][(id(xst), c)] = (remote, epoch)
+            else:
+                launches += comm.exchange(state, remote, geo, group, cbits=xst.cbits, cval=c)
             done = torch.cuda.Event()
             done.record(cs)
             outs.append(done)
@@ -544,7 +602,10 @@ def _remap(state: _State, swaps: list, geo: prog.DeviceGeometry, group, stream) 
     if remote:
         from . import comm
 
-        launches += comm.exchange(state, remote, geo, group)
+        if state.ctx is not None:
+            launches += comm.peer_exchange(state, remote, state.ctx, stream, state.ctx.next_epoch())
+        else:
+            launches += comm.exchange(state, remote, geo, group)
     return launches
 
 
