@@ -319,6 +319,20 @@ def symmetric_buffer(n: int, device, group):
     return buf, PeerContext(me, arena, peers, peer_flags, epoch)
 
 
+_BARRIER: dict = {}
+
+
+def device_barrier(group, device) -> None:
+    """Stream-ordered barrier: a one-element NCCL all-reduce, so work after
+    it starts only once every process has finished the work before it."""
+    import torch.distributed as dist
+
+    t = _BARRIER.get(device)
+    if t is None:
+        t = _BARRIER[device] = torch.zeros(1, dtype=torch.float32, device=device)
+    dist.all_reduce(t, group=group)
+
+
 def swap_args(state, remote: list, me: int, ctx: PeerContext, cbits=None, cval: int = 0):
     """Arguments of svb_peer_swap(_bulk) for one exchange (or its chunk cval
     over `cbits`): process w and peer p = w[e := v] own the pairs

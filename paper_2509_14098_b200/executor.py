@@ -155,12 +155,14 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
     for st in dp.steps:
         steps[st.task_id] = st
     # sweeps launched in parts around an overlapped remap: descriptor ->
-    # {"pre": exchange it feeds, "post": exchange it waits for}
+    # {"pre": exchange it feeds, "post": exchange it waits for,
+    #  "chain": exchange whose depth-first chain starts here}
     overlap = {}
     for st in dp.steps:
         if st.kind == "exchange" and st.cbits and all(ib >= geo.h for ib, _ in st.swaps):
             overlap.setdefault(st.pre, {})["pre"] = st
             overlap.setdefault(st.post, {})["post"] = st
+            overlap.setdefault(st.chain[0], {})["chain"] = st
     out = _Compiled(dev_blob, descs, steps, dp.init_perm, dp.n_fused, time.perf_counter() - t0,
                     host, n_sweeps=len(dp.buf.descs))
     out.overlap = overlap if use_jit else {}
@@ -271,7 +273,8 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
     compiled = None
     norms = None
     events = []  # (kind, start, end)
-    ovl = {"pre": {}, "unpack": {}, "comm": None, "peer": {}}  # overlapped remap events / flags
+    # overlapped remaps: per-chunk events and flag epochs, comm stream, chained sweeps already run
+    ovl = {"pre": {}, "unpack": {}, "comm": None, "peer": {}, "launched": set()}
     fused_order = []  # task ids of executed ApplyFused, in order
 
     def fail(exc):
@@ -474,39 +477,43 @@ def _launch_part(compiled, di, state, norms, grid_limit, stream, cbits, c) -> No
 
 
 def _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, stream, ovl) -> None:
-    """Sweeps of one ApplyFused task; the one before / after an overlapped remap
-    runs in parts linked by events to the remap's chunks on the comm stream."""
+    """Sweeps of one ApplyFused task when remaps overlap the sweeps around
+    them.  A sweep next to an overlapped remap runs in parts, one per chunk;
+    the chain of sweeps before a remap runs depth-first (chunk c of every
+    chain sweep, then an event that lets the remap of chunk c start on the
+    comm stream), and part c of the sweep after it waits for that chunk."""
     from . import comm
 
     grid = min(grid_limit or prog_sms(), OVERLAP_GRID or prog_sms())
+    cur = torch.cuda.current_stream()
     for di in range(st.first, st.first + st.count):
+        if di in ovl["launched"]:
+            continue  # ran earlier as part of a depth-first chain
         roles = compiled.overlap.get(di)
         if not roles:
             _mark(f"sweep{di} start")
             _run_descs(compiled, di, 1, state, rows_eff, L, norms, grid_limit, stream)
             _mark(f"sweep{di} end")
             continue
-        feeds, waits = roles.get("pre"), roles.get("post")
-        cbits = (feeds or waits).cbits  # the planner gives both roles the same chunk bits
-        nparts = 1 << len(cbits)
-        cur = torch.cuda.current_stream()
-        wait_evs = ovl["unpack"].pop(id(waits)) if waits is not None else None
-        evs = []
-        for c in range(nparts):
-            if wait_evs is not None:  # part c needs chunk c of the previous remap
-                cur.wait_event(wait_evs[c])
-                if state.ctx is not None:  # ... swapped on both sides of every pair
-                    remote, epoch = ovl["peer"].pop((id(waits), c))
-                    comm.wait_partners_done(state, remote, state.ctx, cur.cuda_stream, epoch, c)
-            _mark(f"sweep{di}.part{c} start", cur)
-            _launch_part(compiled, di, state, norms, grid, stream, cbits, c)
-            _mark(f"sweep{di}.part{c} end", cur)
-            if feeds is not None:
-                ev = torch.cuda.Event()
-                ev.record(cur)
-                evs.append(ev)
-        if feeds is not None:
-            ovl["pre"][id(feeds)] = evs
+        group = roles["chain"].chain if "chain" in roles else [di]
+        ovl["launched"].update(group)
+        cbits = compiled.cbits[di]  # the planner gives a chain and its remap's post the same bits
+        for c in range(1 << len(cbits)):
+            for dj in group:
+                r = compiled.overlap.get(dj, {})
+                waits, feeds = r.get("post"), r.get("pre")
+                if waits is not None:  # part c needs chunk c of the previous remap ...
+                    cur.wait_event(ovl["unpack"][id(waits)][c])
+                    if state.ctx is not None:  # ... swapped on both sides of every pair
+                        remote, epoch = ovl["peer"][(id(waits), c)]
+                        comm.wait_partners_done(state, remote, state.ctx, cur.cuda_stream, epoch, c)
+                _mark(f"sweep{dj}.part{c} start", cur)
+                _launch_part(compiled, dj, state, norms, grid, stream, cbits, c)
+                _mark(f"sweep{dj}.part{c} end", cur)
+                if feeds is not None:
+                    ev = torch.cuda.Event()
+                    ev.record(cur)
+                    ovl["pre"].setdefault(id(feeds), []).append(ev)
 
 
 def prog_sms() -> int:

@@ -29,6 +29,7 @@ from . import program as prog
 
 CSRC = Path(__file__).resolve().parent / "csrc"
 CACHE_DIR = Path(os.environ.get("SVB200_JIT_CACHE", Path(__file__).resolve().parent.parent / "build" / "jit_cache"))
+MAXREG_OVERLAP = int(os.environ.get("SVB200_JIT_MAXREG_OVERLAP", "232"))
 NVRTC_OPTS = ["--gpu-architecture=sm_100a", "--std=c++17", f"-I{CSRC}", "-lineinfo",
               "--extra-device-vectorization"]
 
@@ -127,7 +128,13 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     w = L.append
     w('#include "sweep_jit.cuh"')
     w(f"// prefetch={os.environ.get('SVB200_JIT_PREFETCH', 'early')}")
-    w(f'extern "C" __global__ void __launch_bounds__({NT}, 1)')
+    # sweeps that run beside an overlapped remap leave each SM sub-partition
+    # room for the remap's one-warp CTA (48 registers): 2 sweep warps per
+    # sub-partition x MAXREG_OVERLAP + 48 must fit in its 16K registers
+    if desc.get("cbits") and MAXREG_OVERLAP:
+        w(f'extern "C" __global__ void __maxnreg__({MAXREG_OVERLAP})')
+    else:
+        w(f'extern "C" __global__ void __launch_bounds__({NT}, 1)')
     w(f"{name}(double2* __restrict__ state, const double2* __restrict__ tab, "
       "const svb_cterm* __restrict__ cterms, const int* __restrict__ cofs, double* __restrict__ norm_out, "
       "const u64 part_val, const u64 part_tid, const long long ntiles) {")

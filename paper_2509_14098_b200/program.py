@@ -542,6 +542,9 @@ class Step:
     cbits: list = field(default_factory=list)
     pre: int = -1  # descriptor of the sweep before the remap
     post: int = -1  # descriptor of the sweep after the remap
+    # sweeps before the remap that run depth-first in parts (oldest first,
+    # ending with `pre`): chunk c of all of them, then chunk c of the remap
+    chain: list = field(default_factory=list)
 
 
 @dataclass
@@ -631,8 +634,16 @@ def _pad_displaced(tile: set, where: list, look: _Lookahead, K: int, L: int) -> 
             tile |= add
 
 
-def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int) -> None:
-    """Chunk bits for remaps whose neighbouring sweeps can run in parts."""
+MAX_CHAIN = 3  # sweeps before a remap that may run depth-first with it
+
+
+def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int, max_chain: int = MAX_CHAIN) -> None:
+    """Chunk bits for remaps whose neighbouring sweeps can run in parts.
+
+    The chunk bits lie outside the tiles of the sweep after the remap, of a
+    chain of up to `max_chain` sweeps before it and of the swapped bits, so
+    every part touches one chunk only: chunk c of the chain, the remap of
+    chunk c and chunk c of the sweep after form one pipeline stage."""
     if nbits <= 0:
         return
     L = geo.L
@@ -641,36 +652,48 @@ def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int) -> None:
             continue
         if any(ib < geo.h for ib, _ in st.swaps):
             continue  # part of the remap is an in-HBM bit swap over all chunks
-        # nearest sweeps on each side; relabel-only leaves (count 0) move no data
-        prev = nxt = None
+        # sweeps on each side, nearest first; relabel-only leaves move no data
+        before = []
         for x in reversed(steps[:i]):
             if x.kind == "exchange":
                 break
-            if x.count:
-                prev = x
-                break
+            before.extend(range(x.first + x.count - 1, x.first - 1, -1))
+        nxt = None
         for x in steps[i + 1:]:
             if x.kind == "exchange":
                 break
             if x.count:
                 nxt = x
                 break
-        if prev is None or nxt is None:
+        if not before or nxt is None:
             continue
-        pre, post = prev.first + prev.count - 1, nxt.first
-        busy = set(buf.descs[pre]["tin"]) | set(buf.descs[post]["tin"]) | {lb for _, lb in st.swaps}
-        have = buf.descs[pre].get("cbits")  # pre is also the post of an earlier remap
+        post = nxt.first
+        if buf.descs[post].get("cbits"):
+            continue
+        busy = set(buf.descs[post]["tin"]) | {lb for _, lb in st.swaps}
+        have = buf.descs[before[0]].get("cbits")  # pre is also the post of an earlier remap
         if have:
-            if busy & set(have) or buf.descs[post].get("cbits"):
+            if busy & set(have) or set(buf.descs[before[0]]["tin"]) & set(have):
                 continue
-            cb = list(have)
+            chain, cb = [before[0]], list(have)
         else:
-            cand = [b for b in range(L - 1, -1, -1) if b not in busy]
-            if not cand or buf.descs[post].get("cbits"):
+            chain, cb = [], None
+            for di in before[:max_chain]:
+                if buf.descs[di].get("cbits") or di == 0:
+                    break  # chunked for an earlier remap / may synthesise |0...0>
+                trial = busy | set(buf.descs[di]["tin"])
+                cand = [b for b in range(L - 1, -1, -1) if b not in trial]
+                if len(cand) < nbits:
+                    break
+                chain.append(di)
+                busy = trial
+                cb = sorted(cand[:nbits])
+            if not chain:
                 continue
-            cb = sorted(cand[:nbits])
-        st.cbits, st.pre, st.post = cb, pre, post
-        buf.descs[pre]["cbits"] = cb
+        st.cbits, st.pre, st.post = cb, chain[0], post
+        st.chain = list(reversed(chain))
+        for di in chain:
+            buf.descs[di]["cbits"] = cb
         buf.descs[post]["cbits"] = cb
 
 
