@@ -1,0 +1,38 @@
+"""Multi-GPU parity (peer-memory remap, overlapped chunks): tools/dist_check.py
+under torchrun on 2 (and 4) GPUs of this box, gathered states vs the golden
+fixtures and the CPU oracle.  Skipped when fewer GPUs are visible."""
+
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("remap", ["peer", "nccl"])
+def test_dist_parity(world, remap):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, SVB200_REMAP=remap)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "tools" / "dist_check.py"),
+           "--quick"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    tail = (r.stdout + r.stderr)[-3000:]
+    assert r.returncode == 0, tail
+    assert "0 mismatches" in r.stdout, tail
