@@ -13,14 +13,16 @@ reported separately in plans/plans.json).
 Workloads (BASELINE.json configs): at N=1 the 34-qubit configs do not fit one
 B200 (256 GiB of complex128), so the single-GPU line is cfg2, QFT-30 with
 hierarchy [30, 12].  For N > 1 the default is weak scaling: QFT-(30+log2 N)
-with [30, 12], 2^30 amplitudes per GPU and one NCCL remap.  ``--workload qv``
-runs QV-30 (N=1) / QV-34 [34-log2 N, 12] (N = 2, 4, 8: strong scaling).
+with [30, 12], 2^30 amplitudes per GPU and one inter-GPU remap.
+``--workload qv`` runs QV-30 (N=1) / QV-34 [34-log2 N, 12] and
+``--workload qft34`` QFT-34 [34-log2 N, 12] (N = 2, 4, 8: strong scaling).
 
 value   = algorithmic HBM bytes of all partition sweeps (32 B x 2^L per
           ApplyFused per rank) / device time of the step,
           summed over ranks; ms_per_step is the circuit time.
 e2e     = the same bytes / time of run_plan(plan, initial=<pinned host
-          state>) plus the device->host copy of the final blocks.
+          rank blocks of this process>) plus the device->host copy of the
+          final blocks (host<->device bytes counted for the whole job).
 roofline= the fused sweep kernel (k_sweep): its algorithmic bytes / its
           CUDA-event time inside the timed steps, against the measured HBM
           copy bandwidth in MEASURED_PEAKS.json.
@@ -44,6 +46,7 @@ METRIC = "circuit time & HBM GB/s, 34q QFT/QV at 1/2/4/8 B200 vs host-CPU refere
 UNIT = "GB/s"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+E2E_HOST_BYTES = 48 << 30  # pinned host buffers per process (in and out each)
 
 
 def workload_name(kind: str, n: int) -> tuple[str, str]:
@@ -52,6 +55,10 @@ def workload_name(kind: str, n: int) -> tuple[str, str]:
         return f"qft{30 + lg}_h30-12", "weak"
     if kind == "qv":
         return ("qv30_h30-12", "strong") if n == 1 else (f"qv34_h{34 - lg}-12", "strong")
+    if kind == "qft34":
+        if n == 1:
+            raise SystemExit("qft34 needs 2+ GPUs: 2^34 complex128 amplitudes are 256 GiB")
+        return f"qft34_h{34 - lg}-12", "strong"
     return kind, "weak"
 
 
@@ -237,9 +244,11 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # each result is dropped before the next run: its state buffer returns to
+    # the pool (at 34 qubits on 2 GPUs one state is 128 GiB of the 180)
     for _ in range(args.warmup):
         res = run_plan(plan)
-    del res
+        del res
     barrier()
 
     # timed region: K full circuits, device-timed with CUDA events
@@ -253,12 +262,12 @@ def main() -> None:
             compute_s += res.stats.compute_seconds + res.stats.layout_seconds
             launches += res.stats.kernel_launches
             sweeps += res.stats.sweeps
+            stats = res.stats
+            del res
         stop.record()
         barrier()
     elapsed = max_over_ranks(start.elapsed_time(stop) / 1e3)
     compute_s = max_over_ranks(compute_s)
-    stats = res.stats
-    del res
 
     total_bytes = plan_bytes(plan)
     value = total_bytes * args.steps / elapsed / 1e9
@@ -269,15 +278,25 @@ def main() -> None:
     sweeps = int(max_over_ranks(float(sweeps)))
     achieved = launch_bytes * sweeps / compute_s / 1e9
 
-    # e2e: initial state from pinned host memory, final blocks back to pinned host
+    # e2e: each process's initial rank blocks (|0...0> at layout phase 0) from
+    # pinned host memory through run_plan(initial=...), final blocks back to
+    # pinned host memory
     torch.cuda.synchronize()
     d = plan.d
+    L = d - plan.g
     e2e = None
-    if (16 << d) <= 40 << 30:
-        host_in = torch.zeros(1 << d, dtype=torch.complex128).pin_memory()
-        host_in[0] = 1.0
-        L = d - plan.g
-        host_out = torch.empty((rows, 1 << L), dtype=torch.complex128).pin_memory()
+    nbytes = 16 * (rows << L)
+    # pinned host buffers of all processes of the node must fit in half its RAM:
+    # separate in/out buffers, else one buffer whose output feeds the next step
+    # (any normalised state is a valid input), else no e2e line
+    host_ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    nbuf = 2 if 2 * local_world * nbytes <= host_ram // 2 else (1 if local_world * nbytes <= host_ram // 2 else 0)
+    if nbuf and nbytes <= E2E_HOST_BYTES:
+        host_in = torch.zeros((rows, 1 << L), dtype=torch.complex128).pin_memory()
+        if rank == 0:
+            host_in[0, 0] = 1.0
+        host_out = torch.empty((rows, 1 << L), dtype=torch.complex128).pin_memory() if nbuf == 2 else host_in
         run_plan(plan, initial=host_in)  # warm
         barrier()
         t0 = time.perf_counter()
@@ -289,7 +308,9 @@ def main() -> None:
         barrier()
         e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
         e2e = {"value": total_bytes / e2e_s / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": 16 << d, "d2h_bytes_per_step": 16 * (rows << L),
+               "h2d_bytes_per_step": world * 16 * (rows << L), "d2h_bytes_per_step": world * 16 * (rows << L),
+               "bytes_note": "whole job: every process copies its own rank blocks in and out"
+                             + ("" if nbuf == 2 else "; one pinned buffer per process, each step's output is the next input"),
                "ms_per_step": 1e3 * e2e_s}
 
     traffic = None

@@ -215,6 +215,98 @@ def _bitperm(src: torch.Tensor, dst: torch.Tensor, perm: list) -> None:
     )
 
 
+def _two_involutions(perm: list) -> tuple[list, list]:
+    """Write a bit permutation (bit r -> perm[r]) as b(a(r)) with a, b
+    involutions: lists of disjoint transpositions, one in-place bitswap each."""
+    n = len(perm)
+    seen = [False] * n
+    a, b = [], []
+    for start in range(n):
+        if seen[start]:
+            continue
+        cyc = [start]
+        seen[start] = True
+        while not seen[perm[cyc[-1]]]:
+            cyc.append(perm[cyc[-1]])
+            seen[cyc[-1]] = True
+        k = len(cyc)
+        if k < 2:
+            continue
+        # a: c_i <-> c_{-i}, b: c_i <-> c_{1-i} (indices mod k), so b(a(c_i)) = c_{i+1}
+        for i in range(k):
+            j = (-i) % k
+            if i < j:
+                a.append((cyc[i], cyc[j]))
+            j = (1 - i) % k
+            if i < j:
+                b.append((cyc[i], cyc[j]))
+    return a, b
+
+
+def _bitswap_pass(state, D: int, pairs: list, stream) -> None:
+    """Disjoint transpositions commute: apply them 8 per svb_bitswap launch."""
+    lib = _native.load()
+    for i in range(0, len(pairs), 8):
+        grp = pairs[i:i + 8]
+        u = np.asarray([x for x, _ in grp], dtype=np.int32)
+        w = np.asarray([y for _, y in grp], dtype=np.int32)
+        _native.check(lib.svb_bitswap(state.buf.data_ptr(), D, u.ctypes.data_as(_native._pi32),
+                                      w.ctypes.data_as(_native._pi32), len(grp), stream), "svb_bitswap")
+
+
+def _initial_blocks(initial, plan, rank_base: int, rows: int, world: int):
+    """This process's rank blocks (rows, 2^L) of `initial` at layout phase 0,
+    in the reference storage order (executor.py:329-343)."""
+    d, g = plan.d, plan.g
+    L = d - g
+    if isinstance(initial, DistState):
+        if initial.phase != 0:
+            raise PlanInvalid(f"initial state is at layout phase {initial.phase}, run_plan starts at 0")
+        initial = initial.blocks
+    t = initial if isinstance(initial, torch.Tensor) else torch.from_numpy(np.asarray(initial))
+    if t.dtype != torch.complex128:
+        t = t.to(torch.complex128)
+    if t.dim() == 2:
+        if tuple(t.shape) == (rows, 1 << L):
+            return t
+        if tuple(t.shape) == (1 << g, 1 << L):
+            return t[rank_base:rank_base + rows]
+        raise DimensionMismatch(f"initial blocks {tuple(t.shape)} != ({rows}, 2^{L}) or (2^{g}, 2^{L})")
+    if tuple(t.shape) != (1 << d,):
+        raise DimensionMismatch(f"state length {tuple(t.shape)} != 2^{d}")
+    # dense basis vector (qubit 0 = MSB): view it with one axis per qubit, order
+    # the axes by storage position, fix this process's top rank bits, and copy
+    # only its 2^(L+h) amplitudes
+    layout = plan.layout_phases[0]
+    q_of_pos = [0] * d
+    for q, pos in enumerate(layout):
+        q_of_pos[pos] = q
+    x = t.reshape((2,) * d).permute(q_of_pos) if d else t
+    h = rows.bit_length() - 1
+    top = g - h
+    for i in range(top):
+        x = x[(rank_base >> (g - 1 - i)) & 1]
+    return x.reshape(rows, 1 << L)
+
+
+def _load_initial(state, initial, plan, rank_base, rows, world, device, local_perm) -> None:
+    """Copy this process's share of `initial` into the state and move its
+    local bits to the planner's initial physical layout in place."""
+    blocks = _initial_blocks(initial, plan, rank_base, rows, world)
+    state.blocks.copy_(blocks, non_blocking=blocks.is_pinned() if blocks.device.type == "cpu" else True)
+    L = state.L
+    perm = [int(p) for p in local_perm]
+    if perm == list(range(L)):
+        return
+    D = L + (rows.bit_length() - 1)
+    if (rows << L) < prog.NREG:
+        D = max(D, 4)
+    a, b = _two_involutions(perm)
+    stream = _stream_ptr(device)
+    _bitswap_pass(state, D, a, stream)
+    _bitswap_pass(state, D, b, stream)
+
+
 class _State:
     """Device storage with a phantom pad so tiny states still fill 16 amplitudes."""
 
@@ -320,9 +412,11 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 if rank_base == 0 and not compiled.zero_init:
                     state.blocks[0, 0] = 1.0  # |0...0> sits at index 0 in every layout
             else:
-                full = scatter(initial, plan, phase=0, device=device, local_perm=compiled.init_perm[:L])
-                state.blocks.copy_(full.blocks[rank_base:rank_base + rows])
-                del full
+                try:
+                    _load_initial(state, initial, plan, rank_base, rows, world, device,
+                                  compiled.init_perm[:L])
+                except (DimensionMismatch, PlanInvalid) as exc:
+                    fail(exc)
             norms = torch.zeros(max(compiled.n_fused, 1), dtype=torch.float64, device=device)
         elif kind == "ApplyFused":
             if state is None:

@@ -476,10 +476,15 @@ def _compile(src: str, name: str) -> bytes:
     image = ctypes.c_void_p()
     size = ctypes.c_size_t()
     log = ctypes.create_string_buffer(1 << 16)
-    rc = lib.svb_jit_compile(src.encode(), name.encode(), len(NVRTC_OPTS), opts, ctypes.byref(image),
-                             ctypes.byref(size), log, len(log))
+    rc = 1
+    for attempt in range(2):  # a failure with an empty log (resource exhaustion) is retried once
+        rc = lib.svb_jit_compile(src.encode(), name.encode(), len(NVRTC_OPTS), opts, ctypes.byref(image),
+                                 ctypes.byref(size), log, len(log))
+        if rc == 0 or log.value.strip():
+            break
     if rc != 0:
-        raise _native.NativeError(f"NVRTC failed for {name}: {log.value.decode(errors='replace')[:4000]}")
+        err = lib.svb_last_error().decode(errors="replace")
+        raise _native.NativeError(f"NVRTC failed for {name} ({err}): {log.value.decode(errors='replace')[:4000]}")
     data = ctypes.string_at(image, size.value)
     lib.svb_jit_free(image)
     try:
@@ -516,7 +521,9 @@ def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: in
         names.append(name)
     _LAST_ZERO_INIT.clear()
     _LAST_ZERO_INIT.update(used)
-    threads = threads or min(32, os.cpu_count() or 4)
+    # the processes of one node compile at the same time: share the host cores
+    local = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    threads = threads or max(1, min(32, (os.cpu_count() or 4) // max(local, 1)))
     with ThreadPoolExecutor(max_workers=threads) as ex:
         cubins = list(ex.map(lambda sn: _compile(*sn), zip(srcs, names)))
     return names, cubins

@@ -64,6 +64,27 @@ def main():
             if err > 1e-10:
                 bad += 1
         n += 1
+    # initial states: the reference's dense vector, and this process's own
+    # phase-0 rank blocks (the distributed form)
+    for name in ["qft20_h18-12", "qv20_h18-12"]:
+        plan = planmod.load(str(ROOT / "plans" / f"{name}.json.gz"))
+        if (1 << plan.g) < world:
+            continue
+        rng = np.random.default_rng(11)
+        v = rng.normal(size=1 << plan.d) + 1j * rng.normal(size=1 << plan.d)
+        v /= np.linalg.norm(v)
+        ref_blocks, _ = orc.run_plan(plan, backend="c", nthreads=8, initial=v)
+        want = orc.gather(ref_blocks, plan.layout_phases[-1], plan.d)
+        rows = (1 << plan.g) // world
+        mine = orc.scatter(v, plan.layout_phases[0], plan.d, plan.g)[me * rows:(me + 1) * rows]
+        for form, init in (("dense", v), ("blocks", torch.from_numpy(np.ascontiguousarray(mine)))):
+            dense = gather(run_plan(plan, initial=init).state)
+            err = float(np.max(np.abs(dense - want)))
+            n += 1
+            if me == 0:
+                print(name, "initial", form, "err", err, flush=True)
+            if err > 1e-10:
+                bad += 1
     if me == 0:
         print(f"dist_check world={world}: {n} runs, {bad} mismatches", flush=True)
     dist.destroy_process_group()
