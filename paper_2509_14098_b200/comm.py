@@ -182,6 +182,8 @@ SWAP_PIECE = int(os.environ.get("SVB200_SWAP_PIECE", "4096"))
 SWAP_STAGES = int(os.environ.get("SVB200_SWAP_STAGES", "3"))
 SWAP_AHEAD = int(os.environ.get("SVB200_SWAP_AHEAD", "1"))
 
+MIN_BULK_RUN = 4096  # contiguous bytes below which the register swap kernel is used
+
 FLAG_RANKS = 64  # flag words: [kind][source rank][chunk], uint32 epochs
 FLAG_CHUNKS = 64
 FLAG_BYTES = 2 * FLAG_RANKS * FLAG_CHUNKS * 4
@@ -389,8 +391,12 @@ def peer_exchange(state, remote: list, ctx: PeerContext, stream, epoch: int, cbi
     ctx.signal(READY, cval, partners, epoch, stream)
     ctx.wait(READY, cval, partners, epoch, stream)
     _mark(f"x{epoch}.{cval} swap start", ts)
-    _native.check(lib.svb_peer_swap_bulk(*args, SWAP_GRID, SWAP_PIECE, SWAP_STAGES, SWAP_AHEAD, stream),
-                  "svb_peer_swap_bulk")
+    run = 16 << min([lb for _, lb in remote] + list(cbits or []))  # bytes per contiguous run
+    if run >= MIN_BULK_RUN:
+        _native.check(lib.svb_peer_swap_bulk(*args, SWAP_GRID, SWAP_PIECE, SWAP_STAGES, SWAP_AHEAD, stream),
+                      "svb_peer_swap_bulk")
+    else:  # short runs: 16-byte register loads/stores from every SM
+        _native.check(lib.svb_peer_swap(*args, 0, 0, stream), "svb_peer_swap")
     _mark(f"x{epoch}.{cval} swap end", ts)
     ctx.signal(DONE, cval, partners, epoch, stream)
     if wait_done:

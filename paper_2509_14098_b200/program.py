@@ -635,6 +635,10 @@ def _pad_displaced(tile: set, where: list, look: _Lookahead, K: int, L: int) -> 
 
 
 MAX_CHAIN = 3  # sweeps before a remap that may run depth-first with it
+# chunk bits and swapped bits of an overlapped remap stay at or above this
+# physical bit: the bulk-copy swap moves contiguous runs of 2^bit amplitudes
+# and needs >= 4 KB pieces to keep NVLink busy (tools/p2p_bench.py)
+MIN_OVERLAP_BIT = 8
 
 
 def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int, max_chain: int = MAX_CHAIN) -> None:
@@ -652,6 +656,8 @@ def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int, max_chain: 
             continue
         if any(ib < geo.h for ib, _ in st.swaps):
             continue  # part of the remap is an in-HBM bit swap over all chunks
+        if min(lb for _, lb in st.swaps) < MIN_OVERLAP_BIT:
+            continue  # short runs: the swap needs the whole GPU (register kernel)
         # sweeps on each side, nearest first; relabel-only leaves move no data
         before = []
         for x in reversed(steps[:i]):
@@ -682,7 +688,7 @@ def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int, max_chain: 
                 if buf.descs[di].get("cbits") or di == 0:
                     break  # chunked for an earlier remap / may synthesise |0...0>
                 trial = busy | set(buf.descs[di]["tin"])
-                cand = [b for b in range(L - 1, -1, -1) if b not in trial]
+                cand = [b for b in range(L - 1, MIN_OVERLAP_BIT - 1, -1) if b not in trial]
                 if len(cand) < nbits:
                     break
                 chain.append(di)
