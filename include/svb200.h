@@ -179,6 +179,19 @@ size_t svb_compare_scratch_bytes(int64_t n);
 int svb_compare(const svb_c128* a, const svb_c128* b, int64_t n, double* out,
                 void* scratch, void* stream);
 
+/* Distributed compare (one shard per process, executor.py:361-372):
+ * svb_shard_argmax: over shard elements i (storage index base + i), the
+ *   largest |a_i||b_i|, ties to the smallest basis index, where perm[s] is
+ *   the basis bit of storage bit s (nbits bits).  out[0] = weight,
+ *   out[1] = basis index (int64 bits), out[2], out[3] = a_k conj(b_k).
+ * svb_shard_maxdev: out[0] = max_i |a_i - phi b_i|.
+ * Both need svb_shard_scratch_bytes(n) bytes of device scratch. */
+size_t svb_shard_scratch_bytes(int64_t n);
+int svb_shard_argmax(const svb_c128* a, const svb_c128* b, int64_t n, uint64_t base, int nbits,
+                     const int32_t* perm, double* out, void* scratch, void* stream);
+int svb_shard_maxdev(const svb_c128* a, const svb_c128* b, int64_t n, double phi_re, double phi_im,
+                     double* out, void* scratch, void* stream);
+
 /* ------------------------------------------------------------------------
  * 5. Run-time specialised sweep kernels (paper_2509_14098_b200/jit.py).
  *

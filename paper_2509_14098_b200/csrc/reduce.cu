@@ -107,6 +107,91 @@ __global__ void k_max_final(const double* dpart, int nparts, double* out) {
   if (threadIdx.x == 0) out[0] = shm[0];
 }
 
+// ---- distributed compare (one shard per process) ---------------------------
+// Shard element i has storage index base + i; its basis index (numpy argmax
+// tie-break) is the bit permutation perm[storage bit] -> basis bit, applied
+// with 8-bit chunk tables.
+struct Perm {
+  int nchunks;
+  uint64_t lut[6 * 256];
+};
+
+struct WI2 {
+  double w;
+  int64_t bi;  // basis index (tie-break)
+  int64_t li;  // shard index
+};
+
+__device__ __forceinline__ WI2 better2(WI2 a, WI2 b) {
+  if (b.w > a.w || (b.w == a.w && b.bi < a.bi)) return b;
+  return a;
+}
+
+__global__ void k_argmax_basis(const double2* __restrict__ a, const double2* __restrict__ b, int64_t n,
+                               uint64_t base, const __grid_constant__ Perm pm, WI2* part) {
+  __shared__ uint64_t lut[6 * 256];
+  for (int i = threadIdx.x; i < pm.nchunks * 256; i += blockDim.x) lut[i] = pm.lut[i];
+  __syncthreads();
+  WI2 best{-1.0, INT64_MAX, 0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t f = base + (uint64_t)i;
+    uint64_t bi = 0;
+    for (int c = 0; c < pm.nchunks; ++c) bi |= lut[c * 256 + ((f >> (8 * c)) & 255)];
+    best = better2(best, WI2{__dmul_rn(cabs_(a[i]), cabs_(b[i])), (int64_t)bi, i});
+  }
+  __shared__ WI2 sh[kThreads];
+  sh[threadIdx.x] = best;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] = better2(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+// out[0] = w, out[1] = basis index (as double bits), out[2..3] = a_k conj(b_k)
+__global__ void k_argmax_final(const double2* __restrict__ a, const double2* __restrict__ b,
+                               const WI2* part, int nparts, double* out) {
+  __shared__ WI2 sh[kThreads];
+  WI2 best{-1.0, INT64_MAX, 0};
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) best = better2(best, part[i]);
+  sh[threadIdx.x] = best;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] = better2(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const WI2 w = sh[0];
+    const double2 ak = a[w.li], bk = b[w.li];
+    out[0] = w.w;
+    reinterpret_cast<int64_t*>(out)[1] = w.bi;
+    out[2] = __dadd_rn(__dmul_rn(ak.x, bk.x), __dmul_rn(ak.y, bk.y));
+    out[3] = __dsub_rn(__dmul_rn(ak.y, bk.x), __dmul_rn(ak.x, bk.y));
+  }
+}
+
+__global__ void k_maxdev_phi(const double2* __restrict__ a, const double2* __restrict__ b, int64_t n,
+                             double2 phi, double* dpart) {
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 bi = b[i], ai = a[i];
+    const double2 pb = make_double2(__dsub_rn(__dmul_rn(phi.x, bi.x), __dmul_rn(phi.y, bi.y)),
+                                    __dadd_rn(__dmul_rn(phi.x, bi.y), __dmul_rn(phi.y, bi.x)));
+    m = fmax(m, cabs_(make_double2(__dsub_rn(ai.x, pb.x), __dsub_rn(ai.y, pb.y))));
+  }
+  __shared__ double shm[kThreads];
+  shm[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) shm[threadIdx.x] = fmax(shm[threadIdx.x], shm[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) dpart[blockIdx.x] = shm[0];
+}
+
 int nblocks(int64_t n) {
   int64_t b = (n + kThreads - 1) / kThreads;
   if (b > kNumSMs * 8) b = kNumSMs * 8;
@@ -149,4 +234,60 @@ extern "C" int svb_compare(const svb_c128* a, const svb_c128* b, int64_t n, doub
   k_max_final<<<1, kThreads, 0, st>>>(dpart, nb, out);
   SVB_CHECK_LAUNCH("svb_compare");
   return SVB_OK;
+}
+
+extern "C" int svb_shard_argmax(const svb_c128* a, const svb_c128* b, int64_t n, uint64_t base, int nbits,
+                                const int32_t* perm, double* out, void* scratch, void* stream) {
+  if (n <= 0 || nbits < 0 || nbits > 48) {
+    set_error("shard_argmax: bad arguments (n=%lld, nbits=%d)", (long long)n, nbits);
+    return SVB_EINVAL;
+  }
+  Perm pm;
+  pm.nchunks = (nbits + 7) / 8;
+  if (pm.nchunks == 0) pm.nchunks = 1;
+  for (int c = 0; c < pm.nchunks; ++c)
+    for (int v = 0; v < 256; ++v) {
+      uint64_t d = 0;
+      for (int j = 0; j < 8; ++j) {
+        const int sb = 8 * c + j;
+        if (sb < nbits && ((v >> j) & 1)) {
+          if (perm[sb] < 0 || perm[sb] >= 64) {
+            set_error("shard_argmax: bad perm entry %d", perm[sb]);
+            return SVB_EINVAL;
+          }
+          d |= uint64_t(1) << perm[sb];
+        }
+      }
+      pm.lut[c * 256 + v] = d;
+    }
+  const int nb = nblocks(n);
+  WI2* part = static_cast<WI2*>(scratch);
+  cudaStream_t st = as_stream(stream);
+  auto A = reinterpret_cast<const double2*>(a);
+  auto B = reinterpret_cast<const double2*>(b);
+  k_argmax_basis<<<nb, kThreads, 0, st>>>(A, B, n, base, pm, part);
+  k_argmax_final<<<1, kThreads, 0, st>>>(A, B, part, nb, out);
+  SVB_CHECK_LAUNCH("svb_shard_argmax");
+  return SVB_OK;
+}
+
+extern "C" int svb_shard_maxdev(const svb_c128* a, const svb_c128* b, int64_t n, double phi_re,
+                                double phi_im, double* out, void* scratch, void* stream) {
+  if (n <= 0) {
+    set_error("shard_maxdev: empty shard");
+    return SVB_EINVAL;
+  }
+  const int nb = nblocks(n);
+  double* dpart = static_cast<double*>(scratch);
+  cudaStream_t st = as_stream(stream);
+  k_maxdev_phi<<<nb, kThreads, 0, st>>>(reinterpret_cast<const double2*>(a),
+                                        reinterpret_cast<const double2*>(b), n,
+                                        make_double2(phi_re, phi_im), dpart);
+  k_max_final<<<1, kThreads, 0, st>>>(dpart, nb, out);
+  SVB_CHECK_LAUNCH("svb_shard_maxdev");
+  return SVB_OK;
+}
+
+extern "C" size_t svb_shard_scratch_bytes(int64_t n) {
+  return sizeof(WI2) * nblocks(n) + 64;
 }

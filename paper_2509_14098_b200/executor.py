@@ -780,8 +780,62 @@ def _as_device_vec(x, device) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(x, dtype=np.complex128).reshape(-1)).to(device)
 
 
+def _same_sharding(a, b) -> bool:
+    return (isinstance(a, DistState) and isinstance(b, DistState) and a.world > 1 and
+            (a.d, a.g, a.world, a.rank_base) == (b.d, b.g, b.world, b.rank_base) and
+            list(a.layouts[a.phase]) == list(b.layouts[b.phase]))
+
+
+def _compare_sharded(a: DistState, b: DistState) -> float:
+    """compare() of two states sharded the same way, without gathering: the
+    phase is taken at the global argmax of |a||b| (ties to the smallest basis
+    index, like numpy's argmax), then the max deviation is all-reduced."""
+    import torch.distributed as dist
+
+    lib = _native.load()
+    A, B = a.blocks.contiguous().view(-1), b.blocks.contiguous().view(-1)
+    device = A.device
+    n = A.numel()
+    d = a.d
+    L = d - a.g
+    layout = a.layouts[a.phase]
+    perm = [0] * d
+    for q in range(d):  # storage bit (LSB-indexed) -> basis bit
+        perm[d - 1 - layout[q]] = d - 1 - q
+    arr, p32 = _native.i32_array(perm)
+    scratch = torch.empty(int(lib.svb_shard_scratch_bytes(n)), dtype=torch.uint8, device=device)
+    out = torch.zeros(4, dtype=torch.float64, device=device)
+    st = _stream_ptr(device)
+    _native.check(lib.svb_shard_argmax(A.data_ptr(), B.data_ptr(), n, a.rank_base << L, d, p32, out.data_ptr(),
+                                       scratch.data_ptr(), st), "svb_shard_argmax")
+    parts = [torch.empty_like(out) for _ in range(a.world)]
+    dist.all_gather(parts, out, group=a.group)
+    best = None
+    for t in parts:
+        w = float(t[0].item())
+        bi = int(t[1:2].view(torch.int64).item())
+        if best is None or w > best[0] or (w == best[0] and bi < best[1]):
+            best = (w, bi, complex(float(t[2].item()), float(t[3].item())))
+    w, _, z = best
+    phi = z / abs(z) if w > 0.0 else 1.0 + 0.0j
+    dev = torch.zeros(1, dtype=torch.float64, device=device)
+    _native.check(lib.svb_shard_maxdev(A.data_ptr(), B.data_ptr(), n, phi.real, phi.imag, dev.data_ptr(),
+                                       scratch.data_ptr(), st), "svb_shard_maxdev")
+    dist.all_reduce(dev, op=dist.ReduceOp.MAX, group=a.group)
+    return float(dev.item())
+
+
 def compare(a, b, device=None) -> float:
-    """Max amplitude deviation after aligning global phase at the largest amplitude."""
+    """Max amplitude deviation after aligning global phase at the largest amplitude.
+
+    Dense vectors as in the reference; two DistStates sharded the same way
+    over several processes are compared shard by shard (no gather)."""
+    if _same_sharding(a, b):
+        return _compare_sharded(a, b)
+    if isinstance(a, DistState):
+        a = gather_device(a)
+    if isinstance(b, DistState):
+        b = gather_device(b)
     if tuple(a.shape) != tuple(b.shape):
         raise DimensionMismatch(f"{tuple(a.shape)} vs {tuple(b.shape)}")
     device = _require_cuda(device if device is not None else (a.device if isinstance(a, torch.Tensor) and a.is_cuda else None))
@@ -796,7 +850,20 @@ def compare(a, b, device=None) -> float:
 
 
 def fidelity(a, b, device=None) -> float:
-    """|<a|b>|^2 / (<a|a><b|b>) on the device."""
+    """|<a|b>|^2 / (<a|a><b|b>) on the device (sharded DistStates: per shard, then all-reduced)."""
+    if _same_sharding(a, b):
+        import torch.distributed as dist
+
+        A, B = a.blocks.reshape(-1), b.blocks.reshape(-1)
+        ov = torch.vdot(A, B)
+        t = torch.stack([ov.real, ov.imag, torch.vdot(A, A).real, torch.vdot(B, B).real])
+        dist.all_reduce(t, group=a.group)
+        re, im, na, nb = (float(x) for x in t.tolist())
+        return (re * re + im * im) / (na * nb)
+    if isinstance(a, DistState):
+        a = gather_device(a)
+    if isinstance(b, DistState):
+        b = gather_device(b)
     device = _require_cuda(device)
     A, B = _as_device_vec(a, device), _as_device_vec(b, device)
     ov = torch.vdot(A, B)

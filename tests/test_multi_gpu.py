@@ -31,7 +31,7 @@ def test_dist_parity(world, remap):
     env = dict(os.environ, SVB200_REMAP=remap)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "tools" / "dist_check.py"),
-           "--quick"]
+           "--quick", "--scale"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     tail = (r.stdout + r.stderr)[-3000:]
     assert r.returncode == 0, tail

@@ -1,7 +1,7 @@
 """Distributed parity check: run plans over N processes (one GPU each, NCCL)
 and compare the gathered state with the CPU oracle.
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/dist_check.py [--quick]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/dist_check.py [--quick] [--scale] [--qft34]
 """
 import gzip
 import json
@@ -19,6 +19,92 @@ import torch.distributed as dist  # noqa: E402
 
 from oracle import oracle as orc  # noqa: E402
 from paper_2509_14098_b200 import gather, plan as planmod, run_plan  # noqa: E402
+
+
+def qft_closed_form_err(state, x: int) -> float:
+    """max |amp - 2^-d/2 exp(-2 pi i x y / 2^d)| over this process's shard,
+    all-reduced; chunked so a 2^33-amplitude shard needs no index array."""
+    d, L = state.d, state.d - state.g
+    layout = state.layouts[state.phase]
+    flat = state.blocks.reshape(-1)
+    n = flat.numel()
+    base = state.rank_base << L
+    mask = (1 << d) - 1
+    lo_bits = min(d, 20)
+    xl, xh = x & ((1 << lo_bits) - 1), x >> lo_bits
+    err = torch.zeros((), dtype=torch.float64, device=flat.device)
+    chunk = 1 << 24
+    for off in range(0, n, chunk):
+        f = torch.arange(off, min(off + chunk, n), device=flat.device, dtype=torch.int64) + base
+        y = torch.zeros_like(f)
+        for q in range(d):  # storage bit d-1-layout[q] -> basis bit d-1-q
+            y |= ((f >> (d - 1 - layout[q])) & 1) << (d - 1 - q)
+        # x*y mod 2^d without int64 overflow: split x into low/high parts
+        r = ((y * xl) + (((y * xh) & ((1 << max(d - lo_bits, 0)) - 1)) << lo_bits)) & mask
+        exp = torch.exp(-2j * np.pi * r.to(torch.float64) / (1 << d)) / 2 ** (d / 2)
+        err = torch.maximum(err, (flat[off:off + f.numel()] - exp).abs().max())
+    dist.all_reduce(err, op=dist.ReduceOp.MAX)
+    return float(err.item())
+
+
+def basis_blocks(plan, x: int, rank_base: int, rows: int, device) -> torch.Tensor:
+    """This process's phase-0 rank blocks of the basis state |x> (device tensor)."""
+    d, g = plan.d, plan.g
+    L = d - g
+    layout = plan.layout_phases[0]
+    f = 0
+    for q in range(d):
+        if (x >> (d - 1 - q)) & 1:
+            f |= 1 << (d - 1 - layout[q])
+    blocks = torch.zeros((rows, 1 << L), dtype=torch.complex128, device=device)
+    if rank_base <= f >> L < rank_base + rows:
+        blocks[(f >> L) - rank_base, f & ((1 << L) - 1)] = 1.0
+    return blocks
+
+
+def scale_checks(me, world):
+    """Full-size parity through size-independent properties, with no gather:
+    QFT of a basis state against its closed form, and sharded compare()."""
+    from paper_2509_14098_b200 import compare, fidelity
+
+    bad = n = 0
+    lg = world.bit_length() - 1
+    names = [(f"qft{30 + lg}_h30-12", 0x2B3C5D1 << lg | 1)]
+    if "--qft34" in sys.argv:
+        names.append((f"qft34_h{34 - lg}-12", 0))
+    for name, x in names:
+        plan = planmod.load(str(ROOT / "plans" / f"{name}.json.gz"))
+        rows = (1 << plan.g) // world
+        init = basis_blocks(plan, x, me * rows, rows, "cuda") if x else None
+        res = run_plan(plan, initial=init)
+        del init
+        err = qft_closed_form_err(res.state, x)
+        n += 1
+        bad += err > 1e-10
+        if me == 0:
+            print(name, "x", hex(x), "closed-form err", err, "remaps", len(res.stats.exchanges), flush=True)
+        del res
+    # sharded compare / fidelity vs the gathered reference compare
+    plan = planmod.load(str(ROOT / "plans" / "qft20_h18-12.json.gz"))
+    if (1 << plan.g) >= world:
+        rng = np.random.default_rng(17)
+        vs = []
+        for _ in range(2):
+            v = rng.normal(size=1 << plan.d) + 1j * rng.normal(size=1 << plan.d)
+            vs.append(v / np.linalg.norm(v))
+        sa, sb = (run_plan(plan, initial=v).state for v in vs)
+        got, fid = compare(sa, sb), fidelity(sa, sb)
+        ga, gb = gather(sa), gather(sb)
+        want = orc.compare(ga, gb)
+        wfid = abs(np.vdot(ga, gb)) ** 2
+        same = compare(sa, sa)
+        n += 1
+        # CUDA's hypot may differ from libm's by an ulp: allow a few ulps
+        ok = abs(got - want) <= 1e-14 * want and abs(fid - wfid) < 1e-12 and same == 0.0
+        bad += not ok
+        if me == 0:
+            print("sharded compare", got, "reference", want, "fidelity", fid, wfid, "self", same, flush=True)
+    return n, bad
 
 
 def main():
@@ -85,6 +171,10 @@ def main():
                 print(name, "initial", form, "err", err, flush=True)
             if err > 1e-10:
                 bad += 1
+    if "--quick" not in sys.argv or "--scale" in sys.argv:
+        n2, bad2 = scale_checks(me, world)
+        n += n2
+        bad += bad2
     if me == 0:
         print(f"dist_check world={world}: {n} runs, {bad} mismatches", flush=True)
     dist.destroy_process_group()
