@@ -511,8 +511,10 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
         group=group,
     )
     histogram = None
-    if shots is not None:
-        histogram = sample(gather(dstate), shots, seed)
+    if shots is not None:  # on the device, shard by shard (no gather)
+        from . import sampling
+
+        histogram = sampling.sample_state(dstate, shots, seed)
     return RunResult(state=dstate, histogram=histogram, stats=stats)
 
 
@@ -870,21 +872,26 @@ def fidelity(a, b, device=None) -> float:
     return float((ov.abs() ** 2 / (torch.vdot(A, A).real * torch.vdot(B, B).real)).item())
 
 
-def sample(dense, shots: int, seed: int | None) -> dict:
-    """Seeded measurement histogram {bitstring: count}, qubit 0 first.
+def sample(dense, shots: int, seed: int | None, device=None) -> dict:
+    """Seeded measurement histogram {bitstring: count}, qubit 0 first
+    (executor.py:375-383), computed on the GPU by ``sampling.sample_state``:
+    the same numpy Generator uniforms and CDF inversion over the basis order.
 
-    Bit-identical to the reference (executor.py:375-383): numpy's Generator
-    draws over |amp|^2 of the gathered vector.
-    """
-    if isinstance(dense, torch.Tensor):
-        dense = dense.cpu().numpy()
-    probs = np.abs(dense) ** 2
-    probs = probs / probs.sum()
-    rng = np.random.default_rng(seed)
-    outcomes = rng.choice(len(dense), size=shots, p=probs)
-    values, counts = np.unique(outcomes, return_counts=True)
-    d = len(dense).bit_length() - 1
-    return {format(int(v), f"0{d}b"): int(c) for v, c in zip(values, counts)}
+    `dense` is a dense vector (host or device) or a DistState (sharded ones
+    are sampled in place, collectively)."""
+    from . import sampling
+
+    if isinstance(dense, DistState):
+        return sampling.sample_state(dense, shots, seed)
+    device = _require_cuda(device if device is not None else
+                           (dense.device if isinstance(dense, torch.Tensor) and dense.is_cuda else None))
+    vec = _as_device_vec(dense, device)
+    n = vec.numel()
+    d = n.bit_length() - 1
+    if n != 1 << d:
+        raise DimensionMismatch(f"state length {n} is not a power of two")
+    st = DistState(blocks=vec.view(1, n), phase=0, d=d, g=0, layouts=[list(range(d))])
+    return sampling.sample_state(st, shots, seed)
 
 
 def oracle_simulate(circuit, device=None) -> np.ndarray:

@@ -104,6 +104,17 @@ def scale_checks(me, world):
         bad += not ok
         if me == 0:
             print("sharded compare", got, "reference", want, "fidelity", fid, wfid, "self", same, flush=True)
+        # sharded device sampling vs numpy's Generator.choice on the gathered state
+        for seed in (3, 4):
+            hist = run_plan(plan, initial=vs[0], shots=5000, seed=seed).histogram
+            p = np.abs(ga) ** 2
+            outc = np.random.default_rng(seed).choice(len(ga), size=5000, p=p / p.sum())
+            vals, cnts = np.unique(outc, return_counts=True)
+            want_h = {format(int(v), f"0{plan.d}b"): int(c) for v, c in zip(vals, cnts)}
+            n += 1
+            bad += hist != want_h
+            if me == 0:
+                print("sharded sample seed", seed, "identical to numpy:", hist == want_h, flush=True)
     return n, bad
 
 
