@@ -210,6 +210,7 @@ class _Arena:
         self.handle = bytes(h)
         self.busy = False
         self.epoch = 0  # last flag value used with this buffer
+        self.last_copy = None  # event of an asynchronous device-to-host copy of the state
 
 
 class _Lease:
@@ -296,6 +297,9 @@ def symmetric_buffer(n: int, device, group):
     if arena is None:
         arena = _Arena(lib, di, nbytes)
         pool.append(arena)
+    elif arena.last_copy is not None:  # a run_plan(out=...) copy may still read it
+        torch.cuda.current_stream(device).wait_event(arena.last_copy)
+        arena.last_copy = None
     buf = torch.as_tensor(_Lease(arena, n), device=device)
     me, world = dist.get_rank(group), dist.get_world_size(group)
     rec = np.frombuffer(arena.handle + int(arena.epoch).to_bytes(8, "little"), dtype=np.uint8)

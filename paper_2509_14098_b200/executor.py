@@ -66,6 +66,13 @@ class RunResult:
     state: DistState
     histogram: dict | None
     stats: RunStats
+    copied: object = None  # CUDA event of the run_plan(out=...) device-to-host copy
+
+    def wait(self) -> "RunResult":
+        """Block until the out= copy of the final blocks has landed."""
+        if self.copied is not None:
+            self.copied.synchronize()
+        return self
 
 
 # ---------------------------------------------------------------------------
@@ -147,7 +154,8 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
     t0 = time.perf_counter()
     dist_run = _dist_info()[1] > 1
     dp = prog.plan_device(plan, geo, rb=JIT_REG_BITS if use_jit else prog.RB,
-                          overlap_bits=_overlap_bits() if (use_jit and dist_run) else 0)
+                          overlap_bits=_overlap_bits() if (use_jit and dist_run) else 0,
+                          free_start=zero_start)
     blob, descs, _ = prog.pack(dp.buf)
     host = np.ascontiguousarray(blob)
     dev_blob = torch.from_numpy(host).to(device)
@@ -293,7 +301,22 @@ def _load_initial(state, initial, plan, rank_base, rows, world, device, local_pe
     """Copy this process's share of `initial` into the state and move its
     local bits to the planner's initial physical layout in place."""
     blocks = _initial_blocks(initial, plan, rank_base, rows, world)
-    state.blocks.copy_(blocks, non_blocking=blocks.is_pinned() if blocks.device.type == "cpu" else True)
+    if blocks.device.type == "cpu" and blocks.is_pinned():
+        # upload on its own stream: it can then run beside an earlier run's
+        # out= download on the copy stream (full-duplex PCIe)
+        up = _UPLOAD_STREAMS.get(device)
+        if up is None:
+            up = _UPLOAD_STREAMS[device] = torch.cuda.Stream(device=device)
+        cur = torch.cuda.current_stream(device)
+        up.wait_stream(cur)
+        with torch.cuda.stream(up):
+            state.blocks.copy_(blocks, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(up)
+        cur.wait_event(ev)
+        state.buf.record_stream(up)
+    else:
+        state.blocks.copy_(blocks, non_blocking=blocks.device.type != "cpu")
     L = state.L
     perm = [int(p) for p in local_perm]
     if perm == list(range(L)):
@@ -331,12 +354,22 @@ class _State:
 # ---------------------------------------------------------------------------
 
 
+_COPY_STREAMS: dict = {}  # device -> stream of run_plan(out=...) downloads
+_UPLOAD_STREAMS: dict = {}  # device -> stream of pinned initial-state uploads
+_FENCE: dict = {}  # device -> one-element tensor (see run_plan(out=...))
+
+
 def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=None, *,
-             device=None, group=None, grid_limit: int = 0, jit=None) -> RunResult:
+             device=None, group=None, grid_limit: int = 0, jit=None, out=None) -> RunResult:
     """Interpret the task list on the GPU(s); returns the final state and optional histogram.
 
     Same contract as ``svpart.executor.run_plan`` (executor.py:179-307).
     Under ``torch.distributed`` every process holds ``2^g / world`` ranks.
+
+    out: optional host tensor (pinned for asynchrony) of this process's
+    rows x 2^L amplitudes.  The final blocks are copied into it on a copy
+    stream and run_plan returns without waiting (``result.wait()`` does), so
+    one circuit's download overlaps the next circuit's upload.
     """
     device = _require_cuda(device)
     lib = _native.load()
@@ -406,7 +439,11 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             # when the first sweep synthesises |0...0> the state needs no memset
             from . import comm
 
-            state = _State(rows, L, device, zero=not compiled.zero_init, group=group,
+            # a memset is needed only when nothing else writes every amplitude:
+            # no |0...0>-synthesising first sweep and no initial state (tiny
+            # states also keep their phantom pad zero)
+            zero = (initial is None and not compiled.zero_init) or (rows << L) < prog.NREG
+            state = _State(rows, L, device, zero=zero, group=group,
                            peer=world > 1 and comm.PEER_MODE == "peer")
             if initial is None:
                 if rank_base == 0 and not compiled.zero_init:
@@ -490,7 +527,9 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
         events.append(("Materialize", e0, e1))
         stats.sweeps += mat.count
         stats.kernel_launches += mat.count
-    torch.cuda.synchronize(device)
+    done = torch.cuda.Event()
+    done.record()
+    done.synchronize()
     if _TRACE and _marks:
         t0 = _marks[0][1]
         stats.trace = [(lab, t0.elapsed_time(ev)) for lab, ev in _marks]
@@ -503,8 +542,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             stats.compute_seconds += sec
         elif kind == "Materialize":
             stats.layout_seconds += sec
-    _check_norms()
-
+    _check_norms()  # small device-to-host reads go before the big out= copy, not behind it
     dstate = DistState(
         blocks=state.blocks, phase=len(plan.layout_phases) - 1, d=d, g=g,
         layouts=[list(p) for p in plan.layout_phases], rank_base=rank_base, world=world,
@@ -515,7 +553,30 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
         from . import sampling
 
         histogram = sampling.sample_state(dstate, shots, seed)
-    return RunResult(state=dstate, histogram=histogram, stats=stats)
+    copied = None
+    if out is not None:
+        if tuple(out.shape) not in ((rows, 1 << L), (rows << L,)) or out.dtype != torch.complex128:
+            raise DimensionMismatch(f"out {tuple(out.shape)} {out.dtype} != ({rows}, 2^{L}) complex128")
+        cs = _COPY_STREAMS.get(device)
+        if cs is None:
+            cs = _COPY_STREAMS[device] = torch.cuda.Stream(device=device)
+        # The drift check's small device-to-host read was the last operation on
+        # this stream; the stream's next operation would then wait behind the
+        # download below in the copy-engine queue (measured, tools/copy_overlap.py).
+        # A one-element kernel in between keeps the next run's upload free to run.
+        fence = _FENCE.get(device)
+        if fence is None:
+            fence = _FENCE[device] = torch.zeros(1, dtype=torch.int32, device=device)
+        fence.zero_()
+        cs.wait_event(done)
+        with torch.cuda.stream(cs):
+            out.view(rows, 1 << L).copy_(state.blocks, non_blocking=True)
+            copied = torch.cuda.Event()
+            copied.record(cs)
+        state.buf.record_stream(cs)  # the allocator keeps the buffer until the copy is done
+        if state.ctx is not None:
+            state.ctx.arena.last_copy = copied  # a pooled peer buffer waits for it before reuse
+    return RunResult(state=dstate, histogram=histogram, stats=stats, copied=copied)
 
 
 _TRACE = os.environ.get("SVB200_TRACE") == "1"

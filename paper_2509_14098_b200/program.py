@@ -705,7 +705,7 @@ def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int, max_chain: 
 
 def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_BITS,
                 max_materialize: int = 64, rb: int = RB, fuse: bool = True,
-                overlap_bits: int = 0) -> DeviceProgram:
+                overlap_bits: int = 0, free_start: bool = True) -> DeviceProgram:
     """Compile every ApplyFused task of a plan for one device, with a global layout.
 
     The physical layout is a permutation `where` of the local bits that the
@@ -715,6 +715,10 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
     materialization sweeps restore the reference layout before the state is
     returned.  The schedule depends only on the plan structure, so every
     device of a distributed run derives the same layouts.
+
+    free_start: the run starts from |0...0> (invariant under any layout), so
+    the planner may pick the initial physical layout; otherwise it starts
+    from the reference layout and an initial state loads with no permutation.
     """
     L, D = geo.L, geo.D
     K = min(kmax, D)
@@ -741,11 +745,12 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
     steps: list = []
     where = list(range(D))
     # the |0...0> start is layout-invariant: pick the first layout like a store
-    look0 = _Lookahead(stream, 0, L)
-    d0 = _choose_store(list(range(L)), where, look0, low, L)
     init = list(where)
-    for r in range(L):
-        init[r] = d0[where[r]]
+    if free_start:
+        look0 = _Lookahead(stream, 0, L)
+        d0 = _choose_store(list(range(L)), where, look0, low, L)
+        for r in range(L):
+            init[r] = d0[where[r]]
     where = list(init)
 
     slot = 0
