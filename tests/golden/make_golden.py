@@ -208,6 +208,10 @@ BENCH = [
     ("mirror_qaoa24_h24-12", lambda: workloads.mirror(workloads.qaoa_maxcut(24, seed=6)), [24, 12]),
     ("mirror_sup24_h21-12", lambda: workloads.mirror(workloads.random_supremacy(24, seed=7)), [21, 12]),
     ("mirror_qv28_h28-12", lambda: workloads.mirror(workloads.quantum_volume(28, seed=8, depth=12)), [28, 12]),
+    # multi-GPU full-size parity (sharded U U^dagger -> |0...0> checks in tools/dist_check.py)
+    ("mirror_qv30_h29-12", lambda: workloads.mirror(workloads.quantum_volume(30, seed=9, depth=12)), [29, 12]),
+    ("mirror_qv31_h29-12", lambda: workloads.mirror(workloads.quantum_volume(31, seed=10, depth=12)), [29, 12]),
+    ("mirror_sup31_h29-12", lambda: workloads.mirror(workloads.random_supremacy(31, seed=11)), [29, 12]),
 ]
 
 

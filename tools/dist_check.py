@@ -84,6 +84,24 @@ def scale_checks(me, world):
         if me == 0:
             print(name, "x", hex(x), "closed-form err", err, "remaps", len(res.stats.exchanges), flush=True)
         del res
+    # mirror circuits U U^dagger over several GPUs (QV with 4-5 remaps, supremacy): every
+    # amplitude must return to |0...0>, checked shard by shard
+    for name in ("mirror_qv30_h29-12", "mirror_qv31_h29-12", "mirror_sup31_h29-12"):
+        plan = planmod.load(str(ROOT / "plans" / f"{name}.json.gz"))
+        if (1 << plan.g) < world:
+            continue
+        res = run_plan(plan)
+        flat = res.state.blocks.reshape(-1)
+        err = (flat.abs().max() if res.state.rank_base else
+               torch.maximum((flat[0] - 1).abs(), flat[1:].abs().max() if flat.numel() > 1 else flat[0].abs() * 0))
+        err = err.to(torch.float64).reshape(1)
+        dist.all_reduce(err, op=dist.ReduceOp.MAX)
+        n += 1
+        bad += float(err.item()) > 1e-10
+        if me == 0:
+            print(name, "mirror |0...0> err", float(err.item()), "remaps", len(res.stats.exchanges),
+                  "ms", round(1e3 * (res.stats.compute_seconds + res.stats.exchange_seconds), 1), flush=True)
+        del res, flat
     # sharded compare / fidelity vs the gathered reference compare
     plan = planmod.load(str(ROOT / "plans" / "qft20_h18-12.json.gz"))
     if (1 << plan.g) >= world:
