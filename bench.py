@@ -292,7 +292,7 @@ def main() -> None:
     host_ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
     nbuf = 2 if 2 * local_world * nbytes <= host_ram // 2 else (1 if local_world * nbytes <= host_ram // 2 else 0)
-    if nbuf and nbytes <= E2E_HOST_BYTES:
+    if nbuf and nbytes <= E2E_HOST_BYTES and args.e2e_steps > 0:
         host_in = torch.zeros((rows, 1 << L), dtype=torch.complex128).pin_memory()
         if rank == 0:
             host_in[0, 0] = 1.0

@@ -35,6 +35,8 @@ import cmath
 import math
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 
 from . import gates as gatelib
@@ -634,7 +636,7 @@ def _pad_displaced(tile: set, where: list, look: _Lookahead, K: int, L: int) -> 
             tile |= add
 
 
-MAX_CHAIN = 3  # sweeps before a remap that may run depth-first with it
+MAX_CHAIN = int(os.environ.get("SVB200_MAX_CHAIN", "3"))  # sweeps before a remap run depth-first with it
 # chunk bits and swapped bits of an overlapped remap stay at or above this
 # physical bit: the bulk-copy swap moves contiguous runs of 2^bit amplitudes
 # and needs >= 4 KB pieces to keep NVLink busy (tools/p2p_bench.py)
