@@ -315,14 +315,15 @@ def main() -> None:
                              + ("" if nbuf == 2 else "; one pinned buffer per process, each step's output is the next input"),
                "ms_per_step": 1e3 * e2e_s}
 
-    traffic = None
+    traffic = fp64 = None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
-            entry = json.loads(prof.read_text()).get(name)
-            traffic = entry["bytes_per_launch"] if entry else None
+            entry = json.loads(prof.read_text()).get(name) or {}
+            traffic = entry.get("bytes_per_launch")
+            fp64 = entry.get("fp64_pipe_pct")
         except Exception:
-            traffic = None
+            traffic = fp64 = None
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
@@ -342,13 +343,24 @@ def main() -> None:
                      "peak_source": f"{peak_kind} hbm_gbs (copy bandwidth, burst)",
                      "bytes_per_launch": launch_bytes,
                      "launches_per_step": sweeps // args.steps,
-                     "launch_ms": 1e3 * compute_s / max(sweeps, 1)},
+                     "launch_ms": 1e3 * compute_s / max(sweeps, 1),
+                     "fp64_pipe_pct": fp64},
         "e2e": e2e,
         "gpu_launches": launches,
         "compile_ms": 1e3 * stats.compile_seconds,
         "exchange_ms": 1e3 * stats.exchange_seconds,
         "clocks": clk.summary(),
     }
+    if world > 1:
+        swap_s = max_over_ranks(stats.swap_seconds)
+        line["nvlink"] = {
+            "bytes_per_direction_per_step": stats.nvlink_bytes,
+            "swap_ms": 1e3 * swap_s,
+            "gbs_per_direction": stats.nvlink_bytes / swap_s / 1e9 if swap_s else None,
+            "peak_gbs_per_direction": 900.0,
+            "note": "per GPU: bytes it sends (= receives) over NVLink per circuit / event-timed swap kernels "
+                    "(max over ranks); overlapped chunks share HBM with the sweeps",
+        }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_line()

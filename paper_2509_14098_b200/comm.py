@@ -374,6 +374,9 @@ def swap_args(state, remote: list, me: int, ctx: PeerContext, cbits=None, cval: 
     return args, [pp.peer for pp in plans], (keep, ptrs)
 
 
+SWAP_TIMES: list = []  # (start, end) events of every swap kernel, drained by run_plan
+
+
 def peer_exchange(state, remote: list, ctx: PeerContext, stream, epoch: int, cbits=None, cval: int = 0,
                   wait_done: bool = True) -> int:
     """One exchange (or chunk `cval` of it) as a flag-ordered bulk swap on
@@ -387,20 +390,23 @@ def peer_exchange(state, remote: list, ctx: PeerContext, stream, epoch: int, cbi
     from .executor import _mark
 
     args, partners, _keep = swap_args(state, remote, ctx.me, ctx, cbits, cval)
-    ts = None
-    if _TRACE_ON():
-        cur = torch.cuda.current_stream()
-        ts = cur if cur.cuda_stream == stream else torch.cuda.ExternalStream(stream)
+    cur = torch.cuda.current_stream()
+    es = cur if cur.cuda_stream == stream else torch.cuda.ExternalStream(stream)
+    ts = es if _TRACE_ON() else None
     _mark(f"x{epoch}.{cval} ready-signal", ts)
     ctx.signal(READY, cval, partners, epoch, stream)
     ctx.wait(READY, cval, partners, epoch, stream)
     _mark(f"x{epoch}.{cval} swap start", ts)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(es)
     run = 16 << min([lb for _, lb in remote] + list(cbits or []))  # bytes per contiguous run
     if run >= MIN_BULK_RUN:
         _native.check(lib.svb_peer_swap_bulk(*args, SWAP_GRID, SWAP_PIECE, SWAP_STAGES, SWAP_AHEAD, stream),
                       "svb_peer_swap_bulk")
     else:  # short runs: 16-byte register loads/stores from every SM
         _native.check(lib.svb_peer_swap(*args, 0, 0, stream), "svb_peer_swap")
+    e1.record(es)
+    SWAP_TIMES.append((e0, e1))
     _mark(f"x{epoch}.{cval} swap end", ts)
     ctx.signal(DONE, cval, partners, epoch, stream)
     if wait_done:

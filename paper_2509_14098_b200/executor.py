@@ -58,6 +58,8 @@ class RunStats:
     sweeps: int = 0
     kernel_launches: int = 0
     layout_seconds: float = 0.0  # trailing sweeps restoring the reference layout
+    swap_seconds: float = 0.0  # inter-GPU swap kernels alone (event-timed, no waits)
+    nvlink_bytes: int = 0  # bytes this process sent over NVLink (= received)
     trace: list = field(default_factory=list)  # (label, ms from run start) with SVB200_TRACE=1
 
 
@@ -498,6 +500,9 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             stats.kernel_launches += launches
             moved = nranks * ((1 << m) - 1) * (1 << (L - m))
             messages = nranks * ((1 << m) - 1)
+            mr = sum(1 for ib, _ in xst.swaps if ib >= geo.h)  # swapped bits that cross GPUs
+            if mr:  # this process's bytes over NVLink (sent = received)
+                stats.nvlink_bytes += 16 * rows * ((1 << mr) - 1) * (1 << (L - mr))
             packed["sent"] = True
             stats.amps_moved += moved
             stats.bytes_moved += moved * 16
@@ -542,6 +547,11 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             stats.compute_seconds += sec
         elif kind == "Materialize":
             stats.layout_seconds += sec
+    from . import comm
+
+    for e0, e1 in comm.SWAP_TIMES:
+        stats.swap_seconds += e0.elapsed_time(e1) / 1e3
+    comm.SWAP_TIMES.clear()
     _check_norms()  # small device-to-host reads go before the big out= copy, not behind it
     dstate = DistState(
         blocks=state.blocks, phase=len(plan.layout_phases) - 1, d=d, g=g,
