@@ -157,3 +157,41 @@ def test_kernel_plugin_matches_numpy():
     big[0, 0] = 1
     kernels.apply_gate(big, np.linalg.qr(rng.normal(size=(128, 128)))[0].astype(complex), list(range(7)))
     assert abs(np.linalg.norm(big) - 1) < 1e-10
+
+
+def test_async_out_download_and_pipelining():
+    """run_plan(out=...) copies the final blocks on a copy stream: the result
+    matches the device state, back-to-back runs with initial/out buffers
+    pipeline correctly, and a wrongly shaped out is rejected."""
+    from pathlib import Path
+
+    import torch
+
+    from paper_2509_14098_b200 import DimensionMismatch, gather, plan as planmod, run_plan
+
+    plan = planmod.load(str(Path(__file__).resolve().parent.parent / "plans" / "qft20_h18-12.json.gz"))
+    L = plan.d - plan.g
+    rows = 1 << plan.g
+    out = torch.empty((rows, 1 << L), dtype=torch.complex128).pin_memory()
+    ref = run_plan(plan)
+    want = ref.state.blocks.cpu()
+    res = run_plan(plan, out=out).wait()
+    assert torch.equal(out, want)
+    # pipelined: each run uploads a different basis state and downloads its QFT
+    outs, runs = [], []
+    for x in (3, 77, 1000):
+        init = torch.zeros(1 << plan.d, dtype=torch.complex128)
+        init[x] = 1.0
+        o = torch.empty((rows, 1 << L), dtype=torch.complex128).pin_memory()
+        runs.append(run_plan(plan, initial=init, out=o))
+        outs.append((x, o))
+    for r, (x, o) in zip(runs, outs):
+        r.wait()
+        dense = gather(r.state)
+        y = np.arange(1 << plan.d)
+        exp = np.exp(-2j * np.pi * ((x * y) % (1 << plan.d)) / (1 << plan.d)) / 2 ** (plan.d / 2)
+        assert np.max(np.abs(dense - exp)) < 1e-12
+        assert torch.equal(o, r.state.blocks.cpu())
+    with pytest.raises(DimensionMismatch):
+        run_plan(plan, out=torch.empty(7, dtype=torch.complex128))
+    del res
