@@ -212,6 +212,7 @@ BENCH = [
     ("mirror_qv30_h29-12", lambda: workloads.mirror(workloads.quantum_volume(30, seed=9, depth=12)), [29, 12]),
     ("mirror_qv31_h29-12", lambda: workloads.mirror(workloads.quantum_volume(31, seed=10, depth=12)), [29, 12]),
     ("mirror_sup31_h29-12", lambda: workloads.mirror(workloads.random_supremacy(31, seed=11)), [29, 12]),
+    ("mirror_qaoa31_h29-12", lambda: workloads.mirror(workloads.qaoa_maxcut(31, seed=12, p=2)), [29, 12]),
 ]
 
 

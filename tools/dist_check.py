@@ -86,7 +86,7 @@ def scale_checks(me, world):
         del res
     # mirror circuits U U^dagger over several GPUs (QV with 4-5 remaps, supremacy): every
     # amplitude must return to |0...0>, checked shard by shard
-    for name in ("mirror_qv30_h29-12", "mirror_qv31_h29-12", "mirror_sup31_h29-12"):
+    for name in ("mirror_qv30_h29-12", "mirror_qv31_h29-12", "mirror_sup31_h29-12", "mirror_qaoa31_h29-12"):
         plan = planmod.load(str(ROOT / "plans" / f"{name}.json.gz"))
         if (1 << plan.g) < world:
             continue
