@@ -156,15 +156,20 @@ def cpu_backend() -> tuple[str, str]:
     return "c", "port"
 
 
-def cpu_baseline_line(steps: int = 1, sample: str = CPU_SAMPLE_PLAN) -> dict:
+def cpu_baseline_line(min_seconds: float = 10.0, sample: str = CPU_SAMPLE_PLAN) -> dict:
+    """The reference's CPU path on a bounded sample: full runs of the sample
+    plan repeated until at least min_seconds of CPU work; value from the mean."""
     plan = load_plan(sample)
     backend, kind = cpu_backend()
-    times = [cpu_reference_step(plan, backend) for _ in range(max(1, steps))]
-    t = min(times)
+    times = []
+    while sum(times) < min_seconds:
+        times.append(cpu_reference_step(plan, backend))
+    t = sum(times) / len(times)
     return {"value": plan_bytes(plan) / t / 1e9, "unit": UNIT, "cores": 1, "kind": kind,
             "sample": f"{sample}: full plan of the same family/hierarchy, reference run_plan "
                       f"semantics with {'the reference _core.pyx kernels' if kind == 'reference' else 'the C port'}"
-                      f", {plan.d} qubits, best of {len(times)} ({t:.2f} s), host cores {os.cpu_count()}",
+                      f", {plan.d} qubits, mean of {len(times)} runs ({t:.2f} s each, {sum(times):.1f} s total), "
+                      f"host cores {os.cpu_count()}, 1 used",
             "seconds": t}
 
 
