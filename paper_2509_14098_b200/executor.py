@@ -332,6 +332,18 @@ def _load_initial(state, initial, plan, rank_base, rows, world, device, local_pe
     _bitswap_pass(state, D, b, stream)
 
 
+class _Flat:
+    """The state as one row of L + log2(rows) bits: the planner may keep a
+    local qubit on a row bit (and a rank bit on a local one), so remote swaps
+    address the whole device index.  Region enumeration is unchanged: rows
+    are simply the top free bits."""
+
+    def __init__(self, state):
+        self.buf, self.ctx = state.buf, state.ctx
+        self.rows = 1
+        self.L = state.L + (state.rows.bit_length() - 1)
+
+
 class _State:
     """Device storage with a phantom pad so tiny states still fill 16 amplitudes."""
 
@@ -707,11 +719,11 @@ def _remap_overlapped(state, xst, geo, group, ovl):
         for c, ev in enumerate(pre_evs):
             cs.wait_event(ev)
             if state.ctx is not None:
-                launches += comm.peer_exchange(state, remote, state.ctx, cs.cuda_stream, epoch,
+                launches += comm.peer_exchange(_Flat(state), remote, state.ctx, cs.cuda_stream, epoch,
                                                cbits=xst.cbits, cval=c, wait_done=False)
                 ovl["peer"][(id(xst), c)] = (remote, epoch)
             else:
-                launches += comm.exchange(state, remote, geo, group, cbits=xst.cbits, cval=c)
+                launches += comm.exchange(_Flat(state), remote, geo, group, cbits=xst.cbits, cval=c)
             done = torch.cuda.Event()
             done.record(cs)
             outs.append(done)
@@ -776,10 +788,11 @@ def _remap(state: _State, swaps: list, geo: prog.DeviceGeometry, group, stream) 
     if remote:
         from . import comm
 
+        flat = _Flat(state)
         if state.ctx is not None:
-            launches += comm.peer_exchange(state, remote, state.ctx, stream, state.ctx.next_epoch())
+            launches += comm.peer_exchange(flat, remote, state.ctx, stream, state.ctx.next_epoch())
         else:
-            launches += comm.exchange(state, remote, geo, group)
+            launches += comm.exchange(flat, remote, geo, group)
     return launches
 
 

@@ -652,7 +652,7 @@ def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int, max_chain: 
     chunk c and chunk c of the sweep after form one pipeline stage."""
     if nbits <= 0:
         return
-    L = geo.L
+    L = geo.L + geo.h  # planner-owned bits (local + rows of this device)
     for i, st in enumerate(steps):
         if st.kind != "exchange" or not st.swaps:
             continue
@@ -741,17 +741,28 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
             leaf_start[task.id] = len(stream)
             stream.extend(prims_of[task.id])
         elif task.kind == "Exchange":
-            stream.append(ExchMark(tuple(L - 1 - s["local_bit"] for s in task.payload["swaps"])))
+            remote_bits = []
+            for s in task.payload["swaps"]:
+                ib = geo.g - 1 - s["rank_bit"]
+                if ib < geo.h:  # rank bit held by this device: a relabel (see below)
+                    stream.append(Swap(L + ib, L - 1 - s["local_bit"]))
+                else:
+                    remote_bits.append(L - 1 - s["local_bit"])
+            stream.append(ExchMark(tuple(remote_bits)))
 
     buf = ProgramBuffers()
     steps: list = []
     where = list(range(D))
+    # bits the planner owns: the local bits and the rank bits held as rows on
+    # this device (phantom pad bits stay put); a remap between a row bit and a
+    # local bit only relabels them
+    NL = L + geo.h
     # the |0...0> start is layout-invariant: pick the first layout like a store
     init = list(where)
     if free_start:
-        look0 = _Lookahead(stream, 0, L)
-        d0 = _choose_store(list(range(L)), where, look0, low, L)
-        for r in range(L):
+        look0 = _Lookahead(stream, 0, NL)
+        d0 = _choose_store(list(range(NL)), where, look0, low, NL)
+        for r in range(NL):
             init[r] = d0[where[r]]
     where = list(init)
 
@@ -763,7 +774,12 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
             sw = []
             for s in task.payload["swaps"]:
                 ib = geo.g - 1 - s["rank_bit"]
-                sw.append((ib, where[L - 1 - s["local_bit"]]))
+                lb = L - 1 - s["local_bit"]
+                if ib < geo.h:  # executor.py:224-281 moves data between rows of this
+                    # device: here only the labels of the two bits swap
+                    where[L + ib], where[lb] = where[lb], where[L + ib]
+                else:
+                    sw.append((ib, where[lb]))
             steps.append(Step("exchange", task.id, swaps=sw))
             continue
         if task.kind != "ApplyFused":
@@ -798,7 +814,7 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
                 j += 1
             # pad the tile with the next qubits needed after this sweep so the
             # store can park them on the low bits
-            look = _Lookahead(stream, base + j, L)
+            look = _Lookahead(stream, base + j, NL)
             tile = set(need)
             for r in sorted(look.first_use, key=look.first_use.get):
                 if len(tile) >= K:
@@ -807,18 +823,18 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
             for r in look.exchange:  # let the store park the next remap's qubits on top
                 if len(tile) + 2 <= K:
                     tile |= {trial[r]}
-            for p_top in range(L - 1, L - 1 - len(look.exchange), -1):
+            for p_top in range(NL - 1, NL - 1 - len(look.exchange), -1):
                 if len(tile) < K:
                     tile.add(p_top)
-            _pad_displaced(tile, trial, look, K, L)
+            _pad_displaced(tile, trial, look, K, NL)
             for b in range(D):
                 if len(tile) >= K:
                     break
                 tile.add(b)
             tile = sorted(tile)
             sp = build_sweep(prims[i:j], tile, where)  # updates `where` (swaps)
-            dest = _choose_store(tile, where, look, low, L)
-            inv = {p: r for r, p in enumerate(where[:L])}
+            dest = _choose_store(tile, where, look, low, NL)
+            inv = {p: r for r, p in enumerate(where[:NL])}
             for p in tile:
                 _, fl = sp.out_map[p]
                 sp.out_map[p] = (dest[p], fl)
@@ -838,12 +854,12 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
     # restore the reference layout
     first = len(buf.descs)
     passes = 0
-    while any(where[r] != r for r in range(L)):
+    while any(where[r] != r for r in range(NL)):
         if passes >= max_materialize:
             raise RuntimeError("layout materialization did not converge")
         passes += 1
         tile = set(range(low))
-        for r in range(L):
+        for r in range(NL):
             if len(tile) + 2 > K:
                 break
             if where[r] != r and (where[r] not in tile or r not in tile):
@@ -855,10 +871,10 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
                 break
             tile.add(b)
         tile = sorted(tile)
-        look = _Lookahead([], 0, L)
+        look = _Lookahead([], 0, NL)
         sp = build_sweep([], tile, where)
-        dest = _choose_store(tile, where, look, 0, L)
-        inv = {p: r for r, p in enumerate(where[:L])}
+        dest = _choose_store(tile, where, look, 0, NL)
+        inv = {p: r for r, p in enumerate(where[:NL])}
         for p in tile:
             sp.out_map[p] = (dest[p], 0)
         for p in tile:
