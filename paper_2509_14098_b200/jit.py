@@ -30,6 +30,8 @@ from . import program as prog
 CSRC = Path(__file__).resolve().parent / "csrc"
 CACHE_DIR = Path(os.environ.get("SVB200_JIT_CACHE", Path(__file__).resolve().parent.parent / "build" / "jit_cache"))
 MAXREG_OVERLAP = int(os.environ.get("SVB200_JIT_MAXREG_OVERLAP", "232"))
+# emit the ops before a stage and its shared-memory stores in two halves (see kernel_source)
+SPLIT_STAGES = os.environ.get("SVB200_JIT_SPLIT", "0") not in ("0", "false", "no")  # measured: no gain
 NVRTC_OPTS = ["--gpu-architecture=sm_100a", "--std=c++17", f"-I{CSRC}", "-lineinfo",
               "--extra-device-vectorization"]
 
@@ -282,15 +284,49 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     cur = None  # current stage index
     if nst == 0:
         slot(0)
+    pending = []  # ops since the last stage
+
+    def flush(half=None):
+        for o in pending:
+            _emit_op(w, o, coef, cur, K, rb, half)
+
+    def split_slot(a_stage, b_stage):
+        """A register slot whose tile bit stays a register bit across the stage
+        and that no pending op pairs on: its two halves go through shared
+        memory independently, so one half's FP64 work can overlap the other
+        half's stores."""
+        if not SPLIT_STAGES:
+            return None
+        ra, rb_ = stage_info[a_stage][0], stage_info[b_stage][0]
+        busy = set()
+        for o in pending:
+            k = int(o["kind"])
+            if k in (prog.OP_H, prog.OP_U1, prog.OP_X):
+                busy.add(int(o["a"]))
+            elif k == prog.OP_U2:
+                busy |= {int(o["a"]), int(o["b"])}
+        for q, tbit in enumerate(ra):
+            if q not in busy and tbit in rb_:
+                return q
+        return None
+
     for op in ops:
         kind = int(op["kind"])
         if kind == prog.OP_STAGE:
             nxt = 0 if cur is None else cur + 1
             if cur is not None:
                 _, _, offs = stage_info[cur]
-                for v in range(NR):
-                    w(f"    tile[sb{cur} ^ {offs[v]}u] = x[{v}];")
+                q = split_slot(cur, nxt)
+                halves = [None] if q is None else [(q, 0), (q, 1)]
+                for hf in halves:
+                    flush(hf)
+                    for v in range(NR):
+                        if hf is None or ((v >> q) & 1) == hf[1]:
+                            w(f"    tile[sb{cur} ^ {offs[v]}u] = x[{v}];")
                 w("    __syncthreads();")
+            else:
+                flush()
+            pending = []
             _, _, offs = stage_info[nxt]
             if nxt == 0 and zero_init:
                 # |0...0>: every amplitude is zero except index 0 of the device
@@ -304,7 +340,9 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
             cur = nxt
             slot(nxt)
             continue
-        _emit_op(w, op, coef, cur, K, rb)
+        pending.append(op)
+    flush()
+    pending = []
 
     if cur is not None:
         _, _, offs = stage_info[cur]
@@ -361,9 +399,16 @@ def _phase_base(w, op, coef_c0: complex, K: int, rb: int) -> None:
             w(f"      if ((t >> {i}) & 1) p = cmul(p, ctab[{int(op['tf']) + i}]);")
 
 
-def _emit_op(w, op, coef, stage, K, rb) -> None:
+def _emit_op(w, op, coef, stage, K, rb, half=None) -> None:
+    """Emit one op; `half` = (register slot, value) restricts it to the
+    amplitudes whose slot bit has that value (ops that do not pair across
+    that slot split exactly into two halves)."""
     NR = 1 << rb
     kind = int(op["kind"])
+
+    def skip(v):
+        return half is not None and ((v >> half[0]) & 1) != half[1]
+
     a = int(op["a"])
     A = 1 << a
     cm, cv = int(op["rmask"]), int(op["b"])
@@ -380,24 +425,24 @@ def _emit_op(w, op, coef, stage, K, rb) -> None:
             _phase_base(w, op, coef[ph], K, rb)
             nt = (int(op["flags"]) >> prog.F_PREG_SHIFT) & 0xF
             fused = kind == prog.OP_H and cm == 0
-            _emit_dfs(w, a, nt, [coef[ph + 1 + s] for s in range(rb)], fused, rb)
+            _emit_dfs(w, a, nt, [coef[ph + 1 + s] for s in range(rb)], fused, rb, half)
         if kind == prog.OP_H and not fused:
             for v in range(NR):
-                if (v & A) or (v & cm) != cv:
+                if (v & A) or (v & cm) != cv or skip(v):
                     continue
                 w(f"      {{ const double2 x0 = x[{v}], x1 = x[{v | A}]; "
                   f"x[{v}] = cadd(x0, x1); x[{v | A}] = csub(x0, x1); }}")
         elif kind == prog.OP_U1:
             m00, m01, m10, m11 = coef[cf:cf + 4]
             for v in range(NR):
-                if (v & A) or (v & cm) != cv:
+                if (v & A) or (v & cm) != cv or skip(v):
                     continue
                 w(f"      {{ const double2 x0 = x[{v}], x1 = x[{v | A}]; "
                   f"x[{v}] = {_lincomb([(m00, 'x0'), (m01, 'x1')])}; "
                   f"x[{v | A}] = {_lincomb([(m10, 'x0'), (m11, 'x1')])}; }}")
     elif kind == prog.OP_X:
         for v in range(NR):
-            if (v & A) or (v & cm) != cv:
+            if (v & A) or (v & cm) != cv or skip(v):
                 continue
             w(f"      {{ const double2 tmp = x[{v}]; x[{v}] = x[{v | A}]; x[{v | A}] = tmp; }}")
     elif kind == prog.OP_U2:
@@ -405,7 +450,7 @@ def _emit_op(w, op, coef, stage, K, rb) -> None:
         B = 1 << b
         M = np.asarray(coef[cf:cf + 16]).reshape(4, 4)
         for v in range(NR):
-            if (v & A) or (v & B):
+            if (v & A) or (v & B) or skip(v):
                 continue
             idx = [v, v | B, v | A, v | A | B]
             w("      {")
@@ -416,21 +461,25 @@ def _emit_op(w, op, coef, stage, K, rb) -> None:
     elif kind == prog.OP_PHALL:
         _phase_base(w, op, coef[cf], K, rb)
         for v in range(NR):
-            w(f"      x[{v}] = cmul(x[{v}], p);")
+            if not skip(v):
+                w(f"      x[{v}] = cmul(x[{v}], p);")
     elif kind == prog.OP_SCALE:
         for v in range(NR):
-            w(f"      x[{v}] = {_cmul_lit(f'x[{v}]', coef[cf])};")
+            if not skip(v):
+                w(f"      x[{v}] = {_cmul_lit(f'x[{v}]', coef[cf])};")
     if pmask:
         w("    }")
     w("    }")
 
 
-def _emit_dfs(w, a: int, nt: int, c: list, fused_h: bool, rb: int) -> None:
+def _emit_dfs(w, a: int, nt: int, c: list, fused_h: bool, rb: int, half=None) -> None:
     """Depth-first product over register slots != a; leaves are amplitudes with bit a set."""
     counter = [0]
 
     def rec(s, v, pv):
         if s == rb:
+            if half is not None and ((v >> half[0]) & 1) != half[1]:
+                return  # the other half (unused partial products are dead code)
             if fused_h:
                 w(f"      {{ const double2 x1 = cmul(x[{v}], {pv}); const double2 x0 = x[{v ^ (1 << a)}]; "
                   f"x[{v ^ (1 << a)}] = cadd(x0, x1); x[{v}] = csub(x0, x1); }}")
