@@ -15,7 +15,8 @@ B200 (256 GiB of complex128), so the single-GPU line is cfg2, QFT-30 with
 hierarchy [30, 12].  For N > 1 the default is weak scaling: QFT-(30+log2 N)
 with [30, 12], 2^30 amplitudes per GPU and one inter-GPU remap.
 ``--workload qv`` runs QV-30 (N=1) / QV-34 [34-log2 N, 12] and
-``--workload qft34`` QFT-34 [34-log2 N, 12] (N = 2, 4, 8: strong scaling).
+``--workload qft34`` QFT-34 [34-log2 N, 12] (N = 2, 4, 8: strong scaling);
+``--workload qaoa`` QAOA-35 [32, 12] (N = 4, 8) and ``--workload sup`` SUP-36 [33, 12] (N = 8).
 
 value   = algorithmic HBM bytes of all partition sweeps (32 B x 2^L per
           ApplyFused per rank) / device time of the step,
@@ -59,6 +60,14 @@ def workload_name(kind: str, n: int) -> tuple[str, str]:
         if n == 1:
             raise SystemExit("qft34 needs 2+ GPUs: 2^34 complex128 amplitudes are 256 GiB")
         return f"qft34_h{34 - lg}-12", "strong"
+    if kind == "qaoa":  # BASELINE cfg4: QAOA-35, 8 ranks of 2^32 amplitudes (64 GiB)
+        if n < 4:
+            raise SystemExit("qaoa (35 qubits, 512 GiB) needs 4+ GPUs")
+        return "qaoa35_h32-12", "strong"
+    if kind == "sup":  # BASELINE cfg5: SUP-36, 8 ranks of 2^33 amplitudes (128 GiB)
+        if n < 8:
+            raise SystemExit("sup (36 qubits, 1 TiB) needs 8 GPUs")
+        return "sup36_h33-12", "strong"
     return kind, "weak"
 
 
