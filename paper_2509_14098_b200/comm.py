@@ -5,13 +5,20 @@ With one process per GPU, a swap of device-id bit e_i with local bit l_i
 (i < m) is a pairwise in-place exchange: process w, whose id reads alpha at
 the e bits, trades its region {local l-bits = v} with peer w[e := v] for
 every v != alpha, and the peer's data lands in that same region (derivation
-in DESIGN.md "Remap").  Regions are not contiguous in general, so each
-chunk is packed into a staging buffer by a CUDA kernel, moved with grouped
-NCCL send/recv (all 2^m - 1 peers in one group), and unpacked; chunks are
-double-buffered so packing chunk c+1 overlaps the transfer of chunk c.
+in DESIGN.md "Remap").  Two implementations:
 
-The data movement functions are injectable so the protocol can be tested
-with the gloo backend on CPU tensors (tests/test_comm_gloo.py).
+* peer memory (default, ``peer_exchange``): the state buffers are allocated
+  symmetrically and mapped into every process with CUDA IPC; one bulk-copy
+  (TMA-engine) kernel swaps each process's half of every pair over NVLink in
+  place, ordered between GPUs by flag words written with stream memory
+  operations, optionally chunk by chunk beside the sweeps;
+* NCCL (``exchange``, SVB200_REMAP=nccl): regions are packed into staging
+  buffers by a CUDA kernel, moved with grouped NCCL send/recv (all 2^m - 1
+  peers in one group) and unpacked, double-buffered by chunk.
+
+The data movement of ``exchange`` is injectable so its protocol can be tested
+with the gloo backend on CPU tensors (tests/test_comm_gloo.py); the peer
+schedule is replayed on CPU in tests/test_peer_schedule.py.
 """
 
 from __future__ import annotations
