@@ -157,7 +157,7 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
     dist_run = _dist_info()[1] > 1
     dp = prog.plan_device(plan, geo, rb=JIT_REG_BITS if use_jit else prog.RB,
                           overlap_bits=_overlap_bits() if (use_jit and dist_run) else 0,
-                          free_start=zero_start)
+                          free_start=zero_start, stable_threads=use_jit and jitmod_shuffle())
     blob, descs, _ = prog.pack(dp.buf)
     host = np.ascontiguousarray(blob)
     dev_blob = torch.from_numpy(host).to(device)
@@ -197,6 +197,12 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
     _compile_cache.clear()  # keep one plan resident
     _compile_cache[key] = (plan, out)
     return out
+
+
+def jitmod_shuffle() -> bool:
+    from . import jit as jitmod
+
+    return jitmod.SHUFFLE_STAGES
 
 
 def _has_remote(st, geo) -> bool:

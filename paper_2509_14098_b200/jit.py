@@ -32,6 +32,8 @@ CACHE_DIR = Path(os.environ.get("SVB200_JIT_CACHE", Path(__file__).resolve().par
 MAXREG_OVERLAP = int(os.environ.get("SVB200_JIT_MAXREG_OVERLAP", "232"))
 # emit the ops before a stage and its shared-memory stores in two halves (see kernel_source)
 SPLIT_STAGES = os.environ.get("SVB200_JIT_SPLIT", "0") not in ("0", "false", "no")  # measured: no gain
+# stage changes that keep the warp-level thread bits move data with warp shuffles
+SHUFFLE_STAGES = os.environ.get("SVB200_JIT_SHUFFLE", "0") not in ("0", "false", "no")  # measured: slower
 NVRTC_OPTS = ["--gpu-architecture=sm_100a", "--std=c++17", f"-I{CSRC}", "-lineinfo",
               "--extra-device-vectorization"]
 
@@ -160,7 +162,11 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     for si, st in enumerate(stages):
         rm = int(st["rmask"])
         regs = [k for k in range(K) if (rm >> k) & 1]
-        comp = [k for k in range(K) if not (rm >> k) & 1]
+        flags = int(st["flags"]) if not isinstance(st, dict) else int(st.get("flags", 0))
+        if flags & prog.F_TORDER:  # thread-bit order chosen by the planner
+            comp = prog.unpack_order(int(st["pval"]), K - len(regs))
+        else:
+            comp = [k for k in range(K) if not (rm >> k) & 1]
         w(f"  const u32 sb{si} = {_xor_img('t', [sw[k] for k in comp])};")
         w(f"  const u64 db{si} = {_deposit('t', [tin[k] for k in comp])};")
         offs = []
@@ -310,10 +316,70 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                 return q
         return None
 
+    def warp_local(a_stage, b_stage):
+        """Changed lane positions [(lane bit, register slot)] when the stage
+        change keeps every warp-level thread bit and each lane that changes
+        receives a tile bit from a register (None otherwise)."""
+        if not SHUFFLE_STAGES or K - rb < 5:
+            return None
+        ra, ca = stage_info[a_stage][0], stage_info[a_stage][1]
+        cb = stage_info[b_stage][1]
+        if ca[5:] != cb[5:]:
+            return None
+        moves = []
+        for p in range(5):
+            if ca[p] != cb[p]:
+                if cb[p] not in ra:
+                    return None
+                moves.append(p)
+        return moves
+
+    def shuffle_stage(a_stage, b_stage, moves):
+        """Butterflies: register slot of tile bit cb[p] <-> lane bit p, then a
+        compile-time renaming to the next stage's register slots."""
+        slots = list(stage_info[a_stage][0])  # slot -> tile bit, updated per butterfly
+        ca, cb = stage_info[a_stage][1], stage_info[b_stage][1]
+        for p in moves:
+            rs = slots.index(cb[p])
+            RS = 1 << rs
+            w("    {")
+            w(f"      const bool up = (t >> {p}) & 1;")
+            for v in range(NR):
+                if v & RS:
+                    continue
+                w(f"      {{ const double2 lo = x[{v}], hi = x[{v | RS}]; const double2 snd = up ? lo : hi; "
+                  f"double2 rcv; rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, {1 << p}); "
+                  f"rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, {1 << p}); "
+                  f"x[{v}] = up ? rcv : lo; x[{v | RS}] = up ? hi : rcv; }}")
+            w("    }")
+            slots[rs] = ca[p]
+        rn = stage_info[b_stage][0]
+        src = []
+        for vn in range(NR):
+            vo = 0
+            for qn in range(rb):
+                if (vn >> qn) & 1:
+                    vo |= 1 << slots.index(rn[qn])
+            src.append(vo)
+        if src != list(range(NR)):
+            w("    {")
+            w(f"      const double2 y[{NR}] = {{" + ", ".join(f"x[{v}]" for v in src) + "};")
+            for v in range(NR):
+                w(f"      x[{v}] = y[{v}];")
+            w("    }")
+
     for op in ops:
         kind = int(op["kind"])
         if kind == prog.OP_STAGE:
             nxt = 0 if cur is None else cur + 1
+            moves = warp_local(cur, nxt) if cur is not None else None
+            if moves is not None:
+                flush()
+                pending = []
+                shuffle_stage(cur, nxt, moves)
+                cur = nxt
+                slot(nxt)
+                continue
             if cur is not None:
                 _, _, offs = stage_info[cur]
                 q = split_slot(cur, nxt)

@@ -49,6 +49,7 @@ NREG = 1 << RB
 OP_STAGE, OP_U1, OP_H, OP_X, OP_U2, OP_PH, OP_PHALL, OP_SCALE = 1, 2, 3, 4, 5, 6, 7, 8
 F_PHASE = 1
 F_PREG_SHIFT = 4
+F_TORDER = 1 << 8  # OP_STAGE: pval holds the stage's thread-bit order (4 bits per thread bit)
 
 OP_DTYPE = np.dtype(
     [
@@ -707,7 +708,7 @@ def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int, max_chain: 
 
 def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_BITS,
                 max_materialize: int = 64, rb: int = RB, fuse: bool = True,
-                overlap_bits: int = 0, free_start: bool = True) -> DeviceProgram:
+                overlap_bits: int = 0, free_start: bool = True, stable_threads: bool = False) -> DeviceProgram:
     """Compile every ApplyFused task of a plan for one device, with a global layout.
 
     The physical layout is a permutation `where` of the local bits that the
@@ -842,7 +843,7 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
                 if p in inv:
                     where[inv[p]] = dest[p]
             sp.norm_slot = slot if j >= n else -1
-            emit_sweep(sp, geo, buf, rb)
+            emit_sweep(sp, geo, buf, rb, stable_threads)
             i = j
             if i >= n:
                 break
@@ -880,7 +881,7 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
         for p in tile:
             if p in inv:
                 where[inv[p]] = dest[p]
-        emit_sweep(sp, geo, buf, rb)
+        emit_sweep(sp, geo, buf, rb, stable_threads)
     if passes:
         steps.append(Step("materialize", None, first, passes))
     return DeviceProgram(buf=buf, steps=steps, init_perm=init, n_fused=slot)
@@ -918,6 +919,51 @@ def _choose_swizzle(K: int, patterns: list, seed: int = 0) -> list:
             lows = base  # correct, only slower
     del low
     return [(1 << k) if k < 3 else ((1 << k) | lows[k]) for k in range(K)]
+
+
+def _thread_orders(stages: list, K: int, stable: bool) -> list:
+    """Tile bit held by each thread bit, per stage.
+
+    Default: ascending tile bits.  `stable` (generated kernels): a tile bit
+    that stays a thread bit keeps its thread-bit position, and the warp-level
+    positions (thread bits >= 5) hold the bits needed last; a stage change
+    that then leaves the warp bits in place moves data within warps only
+    (warp shuffles, no shared memory or barrier; jit.kernel_source)."""
+    n = len(stages)
+
+    def next_use(k, si):
+        for sj in range(si + 1, n):
+            if k in stages[sj][0]:
+                return sj
+        return n + 1
+
+    orders, prev = [], None
+    for si, (rbits_s, _) in enumerate(stages):
+        tb = [k for k in range(K) if k not in rbits_s]
+        if not stable:
+            order = tb
+        elif prev is None:
+            order = sorted(tb, key=lambda k: (next_use(k, si), k))
+        else:
+            order = list(prev)
+            vacated = sorted((p for p, k in enumerate(prev) if k in rbits_s), reverse=True)
+            incoming = sorted((k for k in tb if k not in prev), key=lambda k: (-next_use(k, si), k))
+            for p, k in zip(vacated, incoming):
+                order[p] = k
+        orders.append(order)
+        prev = order
+    return orders
+
+
+def pack_order(order: list) -> int:
+    v = 0
+    for i, k in enumerate(order):
+        v |= int(k) << (4 * i)
+    return v
+
+
+def unpack_order(val: int, n: int) -> list:
+    return [(int(val) >> (4 * i)) & 15 for i in range(n)]
 
 
 def _stages(items: list, rb: int = RB) -> list:
@@ -958,7 +1004,8 @@ class ProgramBuffers:
         return off
 
 
-def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers, rb: int = RB) -> None:
+def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers, rb: int = RB,
+               stable: bool = False) -> None:
     K = sp.K
     tin = sp.tin
     dev_to_tile = {b: k for k, b in enumerate(tin)}
@@ -1004,8 +1051,8 @@ def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers, rb: i
     # smem swizzle: load (tile bits 0..2), store order, each stage's thread bits
     store_order = sorted(range(K), key=lambda k: sp.out_map[tin[k]][0])
     patterns = [[0, 1, 2], store_order[:3]]
-    for rbits_s, _ in stages:
-        comp = [k for k in range(K) if k not in rbits_s]
+    orders = _thread_orders(stages, K, stable)
+    for comp in orders:
         patterns.append(comp[:3])
     sw = _choose_swizzle(K, [p for p in patterns if len(p) == 3])
 
@@ -1019,15 +1066,17 @@ def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers, rb: i
         return s
 
     op_begin = len(buf.ops)
-    for rbits, sitems in stages:
+    for (rbits, sitems), comp in zip(stages, orders):
         rlist = sorted(rbits)
         slot_of = {k: i for i, k in enumerate(rlist)}
-        comp = [k for k in range(K) if k not in rbits]
         tbit_of = {k: i for i, k in enumerate(comp)}
         rmask = 0
         for k in rlist:
             rmask |= 1 << k
-        buf.ops.append(dict(kind=OP_STAGE, rmask=rmask))
+        if stable:
+            buf.ops.append(dict(kind=OP_STAGE, rmask=rmask, flags=F_TORDER, pval=pack_order(comp)))
+        else:
+            buf.ops.append(dict(kind=OP_STAGE, rmask=rmask))
         for it in sitems:
             op = dict(kind=it.kind, a=0, b=0, rmask=0, pmask=0, pval=0, coef=0, tab=-1,
                       ctab=-1, tf=-1, flags=0)

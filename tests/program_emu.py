@@ -79,7 +79,10 @@ def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None)
                         tile[J] = x
                     rm = int(op["rmask"])
                     regs = [k for k in range(K) if (rm >> k) & 1]
-                    comp = [k for k in range(K) if not (rm >> k) & 1]
+                    if int(op["flags"]) & prog.F_TORDER:  # planner-chosen thread-bit order
+                        comp = prog.unpack_order(int(op["pval"]), K - len(regs))
+                    else:
+                        comp = [k for k in range(K) if not (rm >> k) & 1]
                     jt = _dep(tix, comp)
                     jv = _dep(np.arange(NR, dtype=np.int64), regs)
                     jj = jt[:, None] | jv[None, :]
@@ -181,7 +184,7 @@ def _devmap(jt: np.ndarray, tin) -> np.ndarray:
     return out
 
 
-def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog.RB):
+def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog.RB, stable: bool = False):
     """Run a plan through the compiled device programs of `world` devices.
 
     Each device gets its own program (plan_device with its rank range);
@@ -196,7 +199,7 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
     progs, parts = [], []
     for w in range(world):
         geo = prog.DeviceGeometry(d=d, g=g, h=h, rank_base=w * rows, pad_to=prog.RB)
-        dp = prog.plan_device(plan, geo, rb=rb)
+        dp = prog.plan_device(plan, geo, rb=rb, stable_threads=stable)
         blob, descs, p = prog.pack(dp.buf)
         progs.append((geo, dp, descs, p))
     D = progs[0][0].D

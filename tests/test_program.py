@@ -17,12 +17,13 @@ def _cases(grid_docs, grid_states, limit=None, min_ranks=1):
     return out[:limit] if limit else out
 
 
-@pytest.mark.parametrize("rb", [4, 3])
-def test_single_device_programs_match_reference(grid_docs, grid_states, rb):
+@pytest.mark.parametrize("rb,stable", [(4, False), (3, False), (4, True)])
+def test_single_device_programs_match_reference(grid_docs, grid_states, rb, stable):
+    """stable=True: planner-chosen thread-bit orders (the generated kernels' layout)."""
     worst = 0.0
     for doc in _cases(grid_docs, grid_states):
         plan = plan_from_doc(doc["plan"])
-        blocks, norms = program_emu.emulate_plan(plan, rb=rb)
+        blocks, norms = program_emu.emulate_plan(plan, rb=rb, stable=stable)
         err = float(np.max(np.abs(blocks - grid_states[doc["name"]])))
         assert err < TOL, (doc["name"], err)
         assert np.all(np.abs(norms - 1) < 1e-8), doc["name"]
