@@ -32,6 +32,8 @@ CACHE_DIR = Path(os.environ.get("SVB200_JIT_CACHE", Path(__file__).resolve().par
 MAXREG_OVERLAP = int(os.environ.get("SVB200_JIT_MAXREG_OVERLAP", "232"))
 # emit the ops before a stage and its shared-memory stores in two halves (see kernel_source)
 SPLIT_STAGES = os.environ.get("SVB200_JIT_SPLIT", "0") not in ("0", "false", "no")  # measured: no gain
+# per-tile slot tables of tile i+1 are loaded during tile i (off the tile-start critical path)
+CTAB_AHEAD = os.environ.get("SVB200_JIT_CTAB_AHEAD", "1") not in ("0", "false", "no")
 # stage changes that keep the warp-level thread bits move data with warp shuffles
 SHUFFLE_STAGES = os.environ.get("SVB200_JIT_SHUFFLE", "0") not in ("0", "false", "no")  # measured: slower
 NVRTC_OPTS = ["--gpu-architecture=sm_100a", "--std=c++17", f"-I{CSRC}", "-lineinfo",
@@ -245,6 +247,38 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     # Three tile buffers rotate: tile i is computed in buffer i % 3 while the
     # prefetch of tile i+1 and the store of tile i-1 are issued in slices
     # between its stages, so loads, stores and FP64 work overlap.
+    def emit_ctab(tvar, bvar, dst, per_thread):
+        """Per-tile slots of tile `tvar` (origin `bvar`) into `dst`: the
+        product of the LUT entries of its index chunks and residual terms."""
+        lut_off, nch = int(desc["lut_off"]), int(desc["lut_nch"])
+        residual = desc["residual"]
+        w(f"    {{ const long long ftid_ = {full_tid(tvar)};")
+        w(f"    for (int i = t; i < {nct}; i += {NT}) {{")
+        w(f"      const double2* lt = tab + {lut_off} + i * {nch * 256};")
+        w("      double2 acc = __ldg(lt + (ftid_ & 255));")
+        for c in range(1, nch):
+            w(f"      acc = cmul(acc, __ldg(lt + {c * 256} + ((ftid_ >> {8 * c}) & 255)));")
+        emit_residual("i", bvar)
+        w(f"      {dst}[i] = acc;")
+        w("    } }")
+
+    def emit_residual(ivar, bvar):
+        residual = desc["residual"]
+        if any(residual):
+            for s_, terms in enumerate(residual):
+                if not terms:
+                    continue
+                w(f"      if ({ivar} == {s_}) {{")
+                for mask, cval in terms:
+                    w(f"        if (({bvar} & {int(mask)}ull) == {int(mask)}ull) "
+                      f"acc = cmulc(acc, {_lit(cval.real)}, {_lit(cval.imag)});")
+                w("      }")
+
+    if nct and nct <= NT and CTAB_AHEAD:  # slots of this CTA's first tile
+        w("  if (tile_id < ntiles) {")
+        w(f"    const u64 b0c = {origin('tile_id')};")
+        emit_ctab("tile_id", "b0c", "ctab_base", per_thread=False)
+        w("  }")
     if not zero_init:
         w("  if (tile_id < ntiles) {")
         w(f"    const u64 b0 = {origin('tile_id')};")
@@ -263,28 +297,21 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     w(f"    const u64 bn = {origin('nx')};")
     w("    const long long px = tile_id - gridDim.x;")
     w(f"    const u64 bp = {origin('px')};")
-    if nct:
-        lut_off, nch = int(desc["lut_off"]), int(desc["lut_nch"])
-        residual = desc["residual"]
-        w(f"    const long long ftid = {full_tid('tile_id')};")
-        w(f"    for (int i = t; i < {nct}; i += {NT}) {{")
-        w(f"      const double2* lt = tab + {lut_off} + i * {nch * 256};")
-        w("      double2 acc = __ldg(lt + (ftid & 255));")
-        for c in range(1, nch):
-            w(f"      acc = cmul(acc, __ldg(lt + {c * 256} + ((ftid >> {8 * c}) & 255)));")
-        if any(residual):
-            for s_, terms in enumerate(residual):
-                if not terms:
-                    continue
-                w(f"      if (i == {s_}) {{")
-                for mask, cval in terms:
-                    w(f"        if ((base & {int(mask)}ull) == {int(mask)}ull) "
-                      f"acc = cmulc(acc, {_lit(cval.real)}, {_lit(cval.imag)});")
-                w("      }")
-        w("      ctab[i] = acc;")
-        w("    }")
+    ahead = bool(nct) and nct <= NT and CTAB_AHEAD
+    if nct and not ahead:
+        emit_ctab("tile_id", "base", "ctab", per_thread=False)
     w("    cp_async_wait_all();")
     w("    __syncthreads();")
+    if ahead:  # this tile's slots were written at the end of the previous tile
+        w(f"    double2* const ctab_n = ctab_base + ((iter + 1) & 1) * {nct};")
+        lut_off, nch = int(desc["lut_off"]), int(desc["lut_nch"])
+        w(f"    double2 lutn[{nch}];")
+        w(f"    if (has_next && t < {nct}) {{")
+        w(f"      const long long ftn = {full_tid('nx')};")
+        w(f"      const double2* lt = tab + {lut_off} + t * {nch * 256};")
+        for c in range(nch):
+            w(f"      lutn[{c}] = __ldg(lt + {c * 256} + ((ftn >> {8 * c}) & 255));")
+        w("    }")
     w(f"    double2 x[{NR}];")
 
     cur = None  # current stage index
@@ -414,6 +441,15 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
         _, _, offs = stage_info[cur]
         for v in range(NR):
             w(f"    tile[sb{cur} ^ {offs[v]}u] = x[{v}];")
+    if ahead:  # the next tile's slots, from loads issued at the start of this one
+        nch = int(desc["lut_nch"])
+        w(f"    if (has_next && t < {nct}) {{")
+        w("      double2 acc = lutn[0];")
+        for c in range(1, nch):
+            w(f"      acc = cmul(acc, lutn[{c}]);")
+        emit_residual("t", "bn")
+        w("      ctab_n[t] = acc;")
+        w("    }")
     w("  }")
     # the last tile of this CTA is still in shared memory
     w("  __syncthreads();")
