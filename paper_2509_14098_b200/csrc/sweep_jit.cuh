@@ -38,19 +38,3 @@ SVB_F void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memo
 SVB_F void st_stream(double2* p, double2 v) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
-
-// per-tile phase slots: slot i is computed by thread (i % nw) * 32 + i / nw
-// so the work spreads over the warps of the CTA
-SVB_F void tile_slots(double2* ctab, int nct, const svb_cterm* __restrict__ cterms,
-                      const int* __restrict__ cofs, u64 base, int t, int nthreads) {
-  const int nw = nthreads >> 5;
-  const int first = nw ? (t >> 5) + nw * (t & 31) : t;
-  for (int i = first; i < nct; i += nthreads) {
-    double2 acc = make_double2(1.0, 0.0);
-    for (int q = cofs[i]; q < cofs[i + 1]; ++q) {
-      const svb_cterm c = cterms[q];
-      if ((base & c.mask) == c.mask) acc = cmul(acc, make_double2(c.re, c.im));
-    }
-    ctab[i] = acc;
-  }
-}

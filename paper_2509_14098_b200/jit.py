@@ -612,8 +612,19 @@ _LAST_ZERO_INIT: dict = {}  # descriptors the last build_kernels synthesised fro
 _kernels: dict = {}  # (source hash, device) -> kernel handle
 
 
+_HEADER_KEY = None
+
+
+def _header_key() -> str:
+    """Content of the headers the generated source includes (part of the cache key)."""
+    global _HEADER_KEY
+    if _HEADER_KEY is None:
+        _HEADER_KEY = "".join((CSRC / f).read_text() for f in ("sweep_jit.cuh",))
+    return _HEADER_KEY
+
+
 def _compile(src: str, name: str) -> bytes:
-    h = hashlib.sha256((src + "\0" + " ".join(NVRTC_OPTS)).encode()).hexdigest()
+    h = hashlib.sha256((src + "\0" + " ".join(NVRTC_OPTS) + "\0" + _header_key()).encode()).hexdigest()
     hit = _mem_cache.get(h)
     if hit is not None:
         return hit
