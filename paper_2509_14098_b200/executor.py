@@ -480,11 +480,14 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 fail(PlanInvalid("compute before Alloc"))
             st = compiled.steps[task.id]
             slot = len(fused_order)
+            launched = 0
             if st.count and compiled.overlap:
-                _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, stream, ovl)
+                launched = _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, stream,
+                                                 ovl)
             elif st.count:
                 _mark(f"sweeps{st.first}-{st.first + st.count - 1} start")
-                _run_descs(compiled, st.first, st.count, state, rows_eff, L, norms, grid_limit, stream)
+                launched = _run_descs(compiled, st.first, st.count, state, rows_eff, L, norms, grid_limit,
+                                      stream)
                 _mark(f"sweeps{st.first}-{st.first + st.count - 1} end")
             elif slot > 0:  # relabel-only leaf: the state (and its norm) is unchanged
                 norms[slot:slot + 1].copy_(norms[slot - 1:slot])
@@ -492,9 +495,9 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 norms[0:1].fill_(1.0 / world)
             else:
                 lib.svb_norm2(state.buf.data_ptr(), rows << L, norms[slot:].data_ptr(), stream)
-            count = st.count
-            stats.sweeps += count
-            stats.kernel_launches += count
+                launched = 1
+            stats.sweeps += st.count
+            stats.kernel_launches += launched
             fused_order.append(task.id)
         elif kind == "Pack":
             if state is None:
@@ -545,11 +548,11 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
     if mat is not None:  # restore the reference layout
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _run_descs(compiled, mat.first, mat.count, state, rows_eff, L, None, grid_limit, stream)
+        launched = _run_descs(compiled, mat.first, mat.count, state, rows_eff, L, None, grid_limit, stream)
         e1.record()
         events.append(("Materialize", e0, e1))
         stats.sweeps += mat.count
-        stats.kernel_launches += mat.count
+        stats.kernel_launches += launched
     done = torch.cuda.Event()
     done.record()
     done.synchronize()
@@ -661,7 +664,7 @@ def _launch_part(compiled, di, state, norms, grid_limit, stream, cbits, c) -> No
     _native.check(rc, "svb_jit_launch_sweep_part")
 
 
-def _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, stream, ovl) -> None:
+def _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, stream, ovl) -> int:
     """Sweeps of one ApplyFused task when remaps overlap the sweeps around
     them.  A sweep next to an overlapped remap runs in parts, one per chunk;
     the chain of sweeps before a remap runs depth-first (chunk c of every
@@ -671,13 +674,14 @@ def _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, s
 
     grid = min(grid_limit or prog_sms(), OVERLAP_GRID or prog_sms())
     cur = torch.cuda.current_stream()
+    launches = 0
     for di in range(st.first, st.first + st.count):
         if di in ovl["launched"]:
             continue  # ran earlier as part of a depth-first chain
         roles = compiled.overlap.get(di)
         if not roles:
             _mark(f"sweep{di} start")
-            _run_descs(compiled, di, 1, state, rows_eff, L, norms, grid_limit, stream)
+            launches += _run_descs(compiled, di, 1, state, rows_eff, L, norms, grid_limit, stream)
             _mark(f"sweep{di} end")
             continue
         group = roles["chain"].chain if "chain" in roles else [di]
@@ -694,11 +698,13 @@ def _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, s
                         comm.wait_partners_done(state, remote, state.ctx, cur.cuda_stream, epoch, c)
                 _mark(f"sweep{dj}.part{c} start", cur)
                 _launch_part(compiled, dj, state, norms, grid, stream, cbits, c)
+                launches += 1
                 _mark(f"sweep{dj}.part{c} end", cur)
                 if feeds is not None:
                     ev = torch.cuda.Event()
                     ev.record(cur)
                     ovl["pre"].setdefault(id(feeds), []).append(ev)
+    return launches
 
 
 def prog_sms() -> int:
@@ -739,17 +745,19 @@ def _remap_overlapped(state, xst, geo, group, ovl):
 
 
 def _run_descs(compiled, first, count, state, rows_eff, L, norms, grid_limit, stream,
-               skip=()) -> None:
+               skip=()) -> int:
+    """Launch sweeps first .. first+count-1; returns the number of kernel launches."""
     lib = _native.load()
     if not count:
-        return
+        return 0
     descs = compiled.descs[first:first + count]
     nptr = norms.data_ptr() if norms is not None else None
     if compiled.kernels is None:
         rc = lib.svb_run_sweeps(state.buf.data_ptr(), rows_eff, L, compiled.blob.data_ptr(),
                                 descs.ctypes.data, count, nptr, grid_limit, stream)
         _native.check(rc, "svb_run_sweeps")
-        return
+        return count
+    launches = 0
     for i in range(count):
         if first + i in skip:
             continue
@@ -757,11 +765,14 @@ def _run_descs(compiled, first, count, state, rows_eff, L, norms, grid_limit, st
         if cb:  # a kernel compiled for part launches: run all parts in order
             for c in range(1 << len(cb)):
                 _launch_part(compiled, first + i, state, norms, grid_limit, stream, cb, c)
+            launches += 1 << len(cb)
             continue
         rc = lib.svb_jit_launch_sweep(compiled.kernels[first + i], state.buf.data_ptr(),
                                       compiled.blob.data_ptr(), descs[i:i + 1].ctypes.data, nptr,
                                       grid_limit, stream)
         _native.check(rc, "svb_jit_launch_sweep")
+        launches += 1
+    return launches
 
 
 def _remap(state: _State, swaps: list, geo: prog.DeviceGeometry, group, stream) -> int:
