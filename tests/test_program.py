@@ -41,3 +41,51 @@ def test_multi_device_programs_match_reference(grid_docs, grid_states, world):
         assert err < TOL, (doc["name"], world, err)
         n += 1
     assert n > 50
+
+
+def test_two_involutions_compose_to_the_permutation():
+    """executor._two_involutions: any bit permutation as two passes of disjoint
+    transpositions (the in-place initial-state layout change)."""
+    import random
+
+    from paper_2509_14098_b200.executor import _two_involutions
+
+    rng = random.Random(5)
+
+    def apply(pairs, r):
+        for x, y in pairs:
+            if r == x:
+                return y
+            if r == y:
+                return x
+        return r
+
+    for n in range(1, 34):
+        for _ in range(20):
+            perm = list(range(n))
+            rng.shuffle(perm)
+            a, b = _two_involutions(perm)
+            for pairs in (a, b):
+                used = [x for p in pairs for x in p]
+                assert len(used) == len(set(used))
+            assert all(apply(b, apply(a, r)) == perm[r] for r in range(n))
+
+
+def test_stable_thread_orders():
+    """program._thread_orders(stable=True): a tile bit that stays a thread bit
+    keeps its position; warp positions (>= 5) hold the bits needed last."""
+    from paper_2509_14098_b200 import program as prog
+
+    K = 12
+    stages = [[{0, 1, 2, 3}, []], [{0, 1, 4, 5}, []], [{2, 3, 6, 7}, []], [{8, 9, 10, 11}, []]]
+    orders = prog._thread_orders(stages, K, stable=True)
+    for (rbits, _), order in zip(stages, orders):
+        assert sorted(order) == [k for k in range(K) if k not in rbits]
+    for prev, cur in zip(orders, orders[1:]):
+        for p, k in enumerate(prev):
+            if k in cur:
+                assert cur[p] == k
+    # stage 0: bits needed by later stages sit on lanes, never-needed-again ones on warp positions
+    assert set(orders[0][5:]) <= {8, 9, 10, 11}
+    assert prog.unpack_order(prog.pack_order(orders[2]), K - 4) == orders[2]
+    assert prog._thread_orders(stages, K, stable=False)[1] == [2, 3, 6, 7, 8, 9, 10, 11]
