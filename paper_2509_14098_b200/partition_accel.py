@@ -86,19 +86,24 @@ def reach_counts(graph) -> tuple[list, np.ndarray, np.ndarray]:
     ids = graph.topo_order()
     index = {nid: i for i, nid in enumerate(ids)}
     v = len(ids)
-    rows = np.full((v, v), _INF, dtype=np.int64)
+    # int32 rows when safe: a path has fewer than V edges, each of weight
+    # |delta l| <= max l, so with V < 2^15 and max l < 2^15 every distance (and
+    # distance + edge) stays below the 2^30 sentinel; otherwise int64 as the reference
+    small = v * v < (1 << 30) and max((n.l for n in nodes.values()), default=0) < (1 << 15)
+    dt, inf = (np.int32, np.int32(1 << 30)) if small else (np.int64, _INF)
+    rows = np.full((v, v), inf, dtype=dt)
     for nid in reversed(ids):
         row = rows[index[nid]]
         lv = nodes[nid].l
         for u in sorted(nbrs[nid]):
             w = abs(nodes[u].l - lv)
             j = index[u]
-            cand = np.minimum(rows[j] + w, _INF)
+            cand = np.minimum(rows[j] + dt(w), inf)
             cand[j] = w
             np.minimum(row, cand, out=row)
-    hit = rows < _INF
+    hit = rows < inf
     size = hit.sum(axis=1)
-    dist = np.where(hit, rows, 0).sum(axis=1)
+    dist = np.where(hit, rows, 0).sum(axis=1, dtype=np.int64)
     return ids, size, dist
 
 
