@@ -282,6 +282,38 @@ _ARENAS: dict = {}  # device index -> [_Arena]
 _PEER_PTRS: dict = {}  # (device index, peer handle bytes) -> mapped pointer
 
 
+def release_arenas(group=None) -> int:
+    """Free the pooled state buffers no live state uses, and unmap every
+    peer buffer.  Collective over `group` (every process calls it); returns
+    the number of buffers freed here."""
+    import torch.distributed as dist
+
+    from . import _native
+
+    lib = _native.load()
+    torch.cuda.synchronize()
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier(group=group)  # no peer still reads or writes our buffers
+    for (di, _), ptr in list(_PEER_PTRS.items()):
+        with torch.cuda.device(di):
+            _native.check(lib.svb_ipc_close(ptr), "svb_ipc_close")
+    _PEER_PTRS.clear()
+    freed = 0
+    for di, pool in _ARENAS.items():
+        keep = []
+        for a in pool:
+            if a.busy:
+                keep.append(a)
+                continue
+            with torch.cuda.device(di):
+                _native.check(lib.svb_dev_free(a.ptr), "svb_dev_free")
+            freed += 1
+        pool[:] = keep
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier(group=group)
+    return freed
+
+
 def symmetric_buffer(n: int, device, group):
     """A complex128 buffer of n amplitudes on `device` in storage every
     process of `group` has mapped; returns (tensor, PeerContext).

@@ -1,5 +1,5 @@
 """Multi-GPU parity (peer-memory remap, overlapped chunks): tools/dist_check.py
-under torchrun on 2 (and 4) GPUs of this box, gathered states vs the golden
+under torchrun on 2, 4 and 8 GPUs of this box, gathered states vs the golden
 fixtures and the CPU oracle.  Skipped when fewer GPUs are visible."""
 
 import os
@@ -23,7 +23,7 @@ def _port():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("remap", ["peer", "nccl"])
 def test_dist_parity(world, remap):
     if torch.cuda.device_count() < world:

@@ -206,6 +206,11 @@ def main():
         bad += bad2
     if me == 0:
         print(f"dist_check world={world}: {n} runs, {bad} mismatches", flush=True)
+    from paper_2509_14098_b200 import comm
+
+    freed = comm.release_arenas()
+    if me == 0:
+        print(f"released {freed} pooled state buffers", flush=True)
     dist.destroy_process_group()
     sys.exit(1 if bad else 0)
 
