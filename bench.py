@@ -48,6 +48,7 @@ UNIT = "GB/s"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 E2E_HOST_BYTES = 48 << 30  # pinned host buffers per process (in and out each)
+E2E_PIPELINE = os.environ.get("SVB200_E2E_PIPELINE", "1") != "0"  # two circuits in flight
 
 
 def workload_name(kind: str, n: int) -> tuple[str, str]:
@@ -222,7 +223,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="qft")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -314,12 +315,18 @@ def main() -> None:
         run_plan(plan, initial=host_in, out=host_out).wait()  # warm
         barrier()
         t0 = time.perf_counter()
+        prev = None
         for _ in range(args.e2e_steps):
-            # the result's download (copy stream) overlaps the next upload
-            r = run_plan(plan, initial=host_in, out=host_out)
+            # two circuits in flight: this one's upload overlaps the previous
+            # one's compute and download (every copy still runs every step)
+            r = run_plan(plan, initial=host_in, out=host_out, wait=nbuf == 1 or not E2E_PIPELINE)
+            if prev is not None:
+                prev.wait()
+            prev = r
             if nbuf == 1:
                 r.wait()  # one host buffer: the next upload reads what this download writes
-            del r
+        prev.wait()
+        del prev, r
         torch.cuda.synchronize()
         barrier()
         e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)

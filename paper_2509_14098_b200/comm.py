@@ -217,7 +217,7 @@ class _Arena:
         self.handle = bytes(h)
         self.busy = False
         self.epoch = 0  # last flag value used with this buffer
-        self.last_copy = None  # event of an asynchronous device-to-host copy of the state
+        self.last_use = None  # event after the last GPU work of the previous run on this buffer
 
 
 class _Lease:
@@ -249,6 +249,7 @@ class PeerContext:
         self.peer_flags = peer_flags
         self.flags = arena.ptr + arena.nbytes
         self.epoch = epoch
+        self.ready = None  # event the buffer's previous run must reach before it is overwritten
 
     def next_epoch(self) -> int:
         self.epoch += 1
@@ -336,9 +337,10 @@ def symmetric_buffer(n: int, device, group):
     if arena is None:
         arena = _Arena(lib, di, nbytes)
         pool.append(arena)
-    elif arena.last_copy is not None:  # a run_plan(out=...) copy may still read it
-        torch.cuda.current_stream(device).wait_event(arena.last_copy)
-        arena.last_copy = None
+    ready = arena.last_use  # the previous run on this buffer (compute or out= copy) may still use it
+    if ready is not None:
+        torch.cuda.current_stream(device).wait_event(ready)
+        arena.last_use = None
     buf = torch.as_tensor(_Lease(arena, n), device=device)
     me, world = dist.get_rank(group), dist.get_world_size(group)
     rec = np.frombuffer(arena.handle + int(arena.epoch).to_bytes(8, "little"), dtype=np.uint8)
@@ -361,7 +363,9 @@ def symmetric_buffer(n: int, device, group):
             _PEER_PTRS[key] = ptr.value
         peers[r] = _PEER_PTRS[key]
         peer_flags[r] = peers[r] + nbytes
-    return buf, PeerContext(me, arena, peers, peer_flags, epoch)
+    ctx = PeerContext(me, arena, peers, peer_flags, epoch)
+    ctx.ready = ready
+    return buf, ctx
 
 
 _BARRIER: dict = {}

@@ -69,9 +69,14 @@ class RunResult:
     histogram: dict | None
     stats: RunStats
     copied: object = None  # CUDA event of the run_plan(out=...) device-to-host copy
+    _finish: object = field(default=None, repr=False)  # run_plan(wait=False): deferred end of run
 
     def wait(self) -> "RunResult":
-        """Block until the out= copy of the final blocks has landed."""
+        """Finish a run_plan(wait=False) run (timings, drift check) and block
+        until the out= copy of the final blocks has landed."""
+        if self._finish is not None:
+            fin, self._finish = self._finish, None
+            fin()
         if self.copied is not None:
             self.copied.synchronize()
         return self
@@ -311,18 +316,20 @@ def _load_initial(state, initial, plan, rank_base, rows, world, device, local_pe
     blocks = _initial_blocks(initial, plan, rank_base, rows, world)
     if blocks.device.type == "cpu" and blocks.is_pinned():
         # upload on its own stream: it can then run beside an earlier run's
-        # out= download on the copy stream (full-duplex PCIe)
-        up = _UPLOAD_STREAMS.get(device)
-        if up is None:
-            up = _UPLOAD_STREAMS[device] = torch.cuda.Stream(device=device)
+        # out= download (full-duplex PCIe) and an earlier run's compute
+        up = _upload_stream(device)
         cur = torch.cuda.current_stream(device)
-        up.wait_stream(cur)
+        if state.upload_stream is not up and state.ctx is None:
+            up.wait_stream(cur)  # the buffer may still be in use by work on `cur`
+        if state.ctx is not None and state.ctx.ready is not None:
+            up.wait_event(state.ctx.ready)  # a pooled peer buffer's previous run
         with torch.cuda.stream(up):
             state.blocks.copy_(blocks, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(up)
         cur.wait_event(ev)
-        state.buf.record_stream(up)
+        if state.upload_stream is not up:
+            state.buf.record_stream(up)
     else:
         state.blocks.copy_(blocks, non_blocking=blocks.device.type != "cpu")
     L = state.L
@@ -353,20 +360,44 @@ class _Flat:
 class _State:
     """Device storage with a phantom pad so tiny states still fill 16 amplitudes."""
 
-    def __init__(self, rows: int, L: int, device, zero: bool = True, group=None, peer: bool = False):
+    def __init__(self, rows: int, L: int, device, zero: bool = True, group=None, peer: bool = False,
+                 upload_stream=None):
         self.rows, self.L = rows, L
         n = rows << L
         self.ctx = None  # comm.PeerContext of the peer-memory remap
+        self.upload_stream = None  # set when the buffer was allocated for an upload on that stream
         if peer:
             from . import comm
 
             self.buf, self.ctx = comm.symmetric_buffer(max(n, prog.NREG), device, group)
             if zero:
                 self.buf.zero_()
+        elif upload_stream is not None and not zero:
+            # allocated on the upload stream: the caching allocator then only
+            # hands out memory whose earlier users were uploads, so the upload
+            # needs no wait on the compute stream (whose previous circuit may
+            # still be running); the compute stream's use is recorded
+            with torch.cuda.stream(upload_stream):
+                self.buf = torch.empty(max(n, prog.NREG), dtype=torch.complex128, device=device)
+            self.buf.record_stream(torch.cuda.current_stream(device))
+            self.upload_stream = upload_stream
         else:
             alloc = torch.zeros if zero else torch.empty
             self.buf = alloc(max(n, prog.NREG), dtype=torch.complex128, device=device)
         self.blocks = self.buf[:n].view(rows, 1 << L)
+
+
+def _upload_stream(device):
+    up = _UPLOAD_STREAMS.get(device)
+    if up is None:
+        up = _UPLOAD_STREAMS[device] = torch.cuda.Stream(device=device)
+    return up
+
+
+def _pinned_host(x) -> bool:
+    if isinstance(x, DistState):
+        x = x.blocks
+    return isinstance(x, torch.Tensor) and x.device.type == "cpu" and x.dim() == 2 and x.is_pinned()
 
 
 # ---------------------------------------------------------------------------
@@ -377,10 +408,20 @@ class _State:
 _COPY_STREAMS: dict = {}  # device -> stream of run_plan(out=...) downloads
 _UPLOAD_STREAMS: dict = {}  # device -> stream of pinned initial-state uploads
 _FENCE: dict = {}  # device -> one-element tensor (see run_plan(out=...))
+_META_STREAMS: dict = {}  # device -> stream of the deferred drift-check read (run_plan(wait=False))
+_PINNED_POOL: list = []  # pinned float64 readback buffers, returned by each run's finish()
+
+
+def _pinned_take(n: int) -> torch.Tensor:
+    for i, t in enumerate(_PINNED_POOL):
+        if t.numel() >= n:
+            return _PINNED_POOL.pop(i)
+    return torch.empty(max(n, 4096), dtype=torch.float64, pin_memory=True)
 
 
 def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=None, *,
-             device=None, group=None, grid_limit: int = 0, jit=None, out=None) -> RunResult:
+             device=None, group=None, grid_limit: int = 0, jit=None, out=None,
+             wait: bool = True) -> RunResult:
     """Interpret the task list on the GPU(s); returns the final state and optional histogram.
 
     Same contract as ``svpart.executor.run_plan`` (executor.py:179-307).
@@ -390,6 +431,11 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
     rows x 2^L amplitudes.  The final blocks are copied into it on a copy
     stream and run_plan returns without waiting (``result.wait()`` does), so
     one circuit's download overlaps the next circuit's upload.
+
+    wait=False: return as soon as every kernel and copy is enqueued;
+    ``result.wait()`` then finishes the run (event timings, the drift check,
+    which raises NonUnitaryDrift there, and the out= copy), so the next
+    circuit's upload can overlap this one's compute as well.
     """
     device = _require_cuda(device)
     lib = _native.load()
@@ -427,16 +473,17 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
         _check_norms()
         raise exc
 
-    def _check_norms():
+    def _check_norms(vals=None):
         if norms is None or not fused_order:
             return
-        vals = norms.cpu().numpy()
-        if world > 1:
-            t = torch.from_numpy(vals).to(device)
-            import torch.distributed as dist
+        if vals is None:
+            vals = norms.cpu().numpy()
+            if world > 1:
+                t = torch.from_numpy(vals).to(device)
+                import torch.distributed as dist
 
-            dist.all_reduce(t, group=group)
-            vals = t.cpu().numpy()
+                dist.all_reduce(t, group=group)
+                vals = t.cpu().numpy()
         for slot, tid in enumerate(fused_order):
             nv = float(vals[slot])
             if abs(nv - 1.0) > DRIFT_TOL:
@@ -464,7 +511,8 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             # states also keep their phantom pad zero)
             zero = (initial is None and not compiled.zero_init) or (rows << L) < prog.NREG
             state = _State(rows, L, device, zero=zero, group=group,
-                           peer=world > 1 and comm.PEER_MODE == "peer")
+                           peer=world > 1 and comm.PEER_MODE == "peer",
+                           upload_stream=_upload_stream(device) if _pinned_host(initial) else None)
             if initial is None:
                 if rank_base == 0 and not compiled.zero_init:
                     state.blocks[0, 0] = 1.0  # |0...0> sits at index 0 in every layout
@@ -474,7 +522,9 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                                   compiled.init_perm[:L])
                 except (DimensionMismatch, PlanInvalid) as exc:
                     fail(exc)
-            norms = torch.zeros(max(compiled.n_fused, 1), dtype=torch.float64, device=device)
+            # even length: the deferred drift check reads it back in 16-byte units
+            norms = torch.zeros(max(compiled.n_fused, 1) + (max(compiled.n_fused, 1) & 1), dtype=torch.float64,
+                                device=device)
         elif kind == "ApplyFused":
             if state is None:
                 fail(PlanInvalid("compute before Alloc"))
@@ -553,32 +603,73 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
         events.append(("Materialize", e0, e1))
         stats.sweeps += mat.count
         stats.kernel_launches += launched
-    done = torch.cuda.Event()
-    done.record()
-    done.synchronize()
-    if _TRACE and _marks:
-        t0 = _marks[0][1]
-        stats.trace = [(lab, t0.elapsed_time(ev)) for lab, ev in _marks]
-        _marks.clear()
-    for kind, e0, e1 in events:
-        sec = e0.elapsed_time(e1) / 1e3
-        if kind in ("Pack", "Exchange", "Unpack"):
-            stats.exchange_seconds += sec
-        elif kind == "ApplyFused":
-            stats.compute_seconds += sec
-        elif kind == "Materialize":
-            stats.layout_seconds += sec
+    fin_ev = torch.cuda.Event()
+    fin_ev.record()
     from . import comm
 
-    for e0, e1 in comm.SWAP_TIMES:
-        stats.swap_seconds += e0.elapsed_time(e1) / 1e3
+    swap_events = list(comm.SWAP_TIMES)  # this run's swaps (another run may start before it finishes)
     comm.SWAP_TIMES.clear()
-    _check_norms()  # small device-to-host reads go before the big out= copy, not behind it
+    norm_host = norm_ev = None
+    if not wait and norms is not None and fused_order:
+        # deferred drift check: reduce on the device now, read back on a side
+        # stream, so no small copy ever queues on this stream behind a download
+        nsum = norms
+        if world > 1:
+            import torch.distributed as dist
+
+            nsum = norms.clone()
+            dist.all_reduce(nsum, group=group)
+        src_ev = torch.cuda.Event()
+        src_ev.record()
+        ms = _META_STREAMS.get(device)
+        if ms is None:
+            ms = _META_STREAMS[device] = torch.cuda.Stream(device=device)
+        ms.wait_event(src_ev)
+        norm_host = _pinned_take(nsum.numel())  # pooled: a fresh pinned allocation syncs the device
+        with torch.cuda.stream(ms):
+            # an SM copy straight into mapped pinned memory: a copy-engine
+            # transfer would queue behind the out= downloads of this and the
+            # next circuit (measured, tools/pipeline_probe.py)
+            _native.check(lib.svb_copy(norm_host.data_ptr(), nsum.data_ptr(), nsum.numel() // 2, 1, ms.cuda_stream),
+                          "svb_copy")
+            norm_ev = torch.cuda.Event()
+            norm_ev.record(ms)
+        nsum.record_stream(ms)
+
+    def finish():
+        """Host side of the end of the run: event timings and the drift check."""
+        fin_ev.synchronize()
+        if _TRACE and _marks:
+            t0 = _marks[0][1]
+            stats.trace = [(lab, t0.elapsed_time(ev)) for lab, ev in _marks]
+            _marks.clear()
+        for kind, e0, e1 in events:
+            sec = e0.elapsed_time(e1) / 1e3
+            if kind in ("Pack", "Exchange", "Unpack"):
+                stats.exchange_seconds += sec
+            elif kind == "ApplyFused":
+                stats.compute_seconds += sec
+            elif kind == "Materialize":
+                stats.layout_seconds += sec
+        for e0, e1 in swap_events:
+            stats.swap_seconds += e0.elapsed_time(e1) / 1e3
+        if norm_ev is not None:
+            norm_ev.synchronize()
+            vals = norm_host.numpy().copy()
+            _PINNED_POOL.append(norm_host)
+            _check_norms(vals)
+        else:
+            _check_norms()
+
     dstate = DistState(
         blocks=state.blocks, phase=len(plan.layout_phases) - 1, d=d, g=g,
         layouts=[list(p) for p in plan.layout_phases], rank_base=rank_base, world=world,
         group=group,
     )
+    if not wait and shots is not None:
+        raise ValueError("run_plan(shots=...) needs wait=True")
+    if wait:
+        finish()  # small device-to-host reads go before the big out= copy, not behind it
     histogram = None
     if shots is not None:  # on the device, shard by shard (no gather)
         from . import sampling
@@ -599,15 +690,18 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
         if fence is None:
             fence = _FENCE[device] = torch.zeros(1, dtype=torch.int32, device=device)
         fence.zero_()
-        cs.wait_event(done)
+        cs.wait_event(fin_ev)
         with torch.cuda.stream(cs):
             out.view(rows, 1 << L).copy_(state.blocks, non_blocking=True)
             copied = torch.cuda.Event()
             copied.record(cs)
         state.buf.record_stream(cs)  # the allocator keeps the buffer until the copy is done
-        if state.ctx is not None:
-            state.ctx.arena.last_copy = copied  # a pooled peer buffer waits for it before reuse
-    return RunResult(state=dstate, histogram=histogram, stats=stats, copied=copied)
+    if state.ctx is not None:  # a pooled peer buffer's next user waits for this run's last use
+        state.ctx.arena.last_use = copied if copied is not None else fin_ev
+    res = RunResult(state=dstate, histogram=histogram, stats=stats, copied=copied)
+    if not wait:
+        res._finish = finish
+    return res
 
 
 _TRACE = os.environ.get("SVB200_TRACE") == "1"

@@ -195,3 +195,29 @@ def test_async_out_download_and_pipelining():
     with pytest.raises(DimensionMismatch):
         run_plan(plan, out=torch.empty(7, dtype=torch.complex128))
     del res
+
+
+def test_deferred_finish_pipelining_and_drift():
+    """run_plan(wait=False): results and stats complete at wait(); a drifted
+    initial state raises NonUnitaryDrift from wait()."""
+    from pathlib import Path
+
+    import torch
+
+    from paper_2509_14098_b200 import NonUnitaryDrift, plan as planmod, run_plan
+
+    plan = planmod.load(str(Path(__file__).resolve().parent.parent / "plans" / "qft20_h18-12.json.gz"))
+    rows, L = 1 << plan.g, plan.d - plan.g
+    want = run_plan(plan).state.blocks.cpu()
+    outs = [torch.empty((rows, 1 << L), dtype=torch.complex128).pin_memory() for _ in range(3)]
+    runs = [run_plan(plan, out=o, wait=False) for o in outs]
+    for r, o in zip(runs, outs):
+        r.wait()
+        assert torch.equal(o, want)
+        assert r.stats.compute_seconds > 0
+    bad = np.full(1 << plan.d, 0.5, dtype=complex)
+    r = run_plan(plan, initial=bad, wait=False)
+    with pytest.raises(NonUnitaryDrift):
+        r.wait()
+    with pytest.raises(ValueError):
+        run_plan(plan, shots=10, wait=False)

@@ -70,12 +70,22 @@ ex._State = State
 run_plan(plan, initial=host_in, out=host_out).wait()
 torch.cuda.synchronize()
 T0.record()
+import os as _os  # noqa: E402
+ASYNC = _os.environ.get("PROBE_ASYNC") == "1"
 rs = []
+prev = None
 for i in range(3):
     t = time.perf_counter()
     eb = torch.cuda.Event(enable_timing=True)
     eb.record()
-    r = run_plan(plan, initial=host_in, out=host_out)
+    r = run_plan(plan, initial=host_in, out=host_out, wait=not ASYNC)
+    t_call = time.perf_counter()
+    if ASYNC:
+        if prev is not None:
+            prev.wait()
+        prev = r
+    marks.append((f"step {i} run_plan host ms", 1e3 * (t_call - t)))
+    marks.append((f"step {i} prev.wait host ms", 1e3 * (time.perf_counter() - t_call)))
     ea = torch.cuda.Event(enable_timing=True)
     ea.record()
     marks.append((f"step {i} start", eb, eb))
@@ -86,6 +96,9 @@ for i in range(3):
     marks.append((f"step {i} host ms", 1e3 * (time.perf_counter() - t)))
     cs = ex._COPY_STREAMS[torch.device("cuda", 0)] if torch.device("cuda", 0) in ex._COPY_STREAMS else list(ex._COPY_STREAMS.values())[0]
     rs.append(r.copied)
+    ec2 = torch.cuda.Event(enable_timing=True)
+    ec2.record(list(ex._COPY_STREAMS.values())[0])
+    marks.append((f"step {i} copy-stream tail (incl. this D2H)", ec2, ec2))
     del r
     ed = torch.cuda.Event(enable_timing=True)
     ed.record()
