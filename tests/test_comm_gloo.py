@@ -79,6 +79,8 @@ def _worker(rank, world, port, L, rows, remote, chunk, q):
     (2, 2, 5, [(0, 0)], 64),
     (4, 1, 6, [(0, 2), (1, 4)], 5),
     (4, 2, 5, [(1, 1), (0, 3)], 1000),
+    (8, 1, 6, [(0, 3), (1, 4), (2, 5)], 3),
+    (8, 2, 5, [(2, 0), (0, 4), (1, 2)], 1000),
 ])
 def test_exchange_matches_bit_swap(world, rows, L, remote, chunk):
     ctx = mp.get_context("spawn")
