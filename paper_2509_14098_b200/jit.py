@@ -34,6 +34,7 @@ MAXREG_OVERLAP = int(os.environ.get("SVB200_JIT_MAXREG_OVERLAP", "232"))
 SPLIT_STAGES = os.environ.get("SVB200_JIT_SPLIT", "0") not in ("0", "false", "no")  # measured: no gain
 # per-tile slot tables of tile i+1 are loaded during tile i (off the tile-start critical path)
 CTAB_AHEAD = os.environ.get("SVB200_JIT_CTAB_AHEAD", "1") not in ("0", "false", "no")
+NO_AHEAD_ZERO = os.environ.get("SVB200_JIT_NO_AHEAD_ZERO", "1") not in ("0", "false", "no")
 # stage changes that keep the warp-level thread bits move data with warp shuffles
 SHUFFLE_STAGES = os.environ.get("SVB200_JIT_SHUFFLE", "0") not in ("0", "false", "no")  # measured: slower
 NVRTC_OPTS = ["--gpu-architecture=sm_100a", "--std=c++17", f"-I{CSRC}", "-lineinfo",
@@ -274,7 +275,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                       f"acc = cmulc(acc, {_lit(cval.real)}, {_lit(cval.imag)});")
                 w("      }")
 
-    if nct and nct <= NT and CTAB_AHEAD:  # slots of this CTA's first tile
+    if nct and nct <= NT and CTAB_AHEAD and not (zero_init and NO_AHEAD_ZERO):  # slots of this CTA's first tile
         w("  if (tile_id < ntiles) {")
         w(f"    const u64 b0c = {origin('tile_id')};")
         emit_ctab("tile_id", "b0c", "ctab_base", per_thread=False)
@@ -297,7 +298,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     w(f"    const u64 bn = {origin('nx')};")
     w("    const long long px = tile_id - gridDim.x;")
     w(f"    const u64 bp = {origin('px')};")
-    ahead = bool(nct) and nct <= NT and CTAB_AHEAD
+    ahead = bool(nct) and nct <= NT and CTAB_AHEAD and not (zero_init and NO_AHEAD_ZERO)
     if nct and not ahead:
         emit_ctab("tile_id", "base", "ctab", per_thread=False)
     w("    cp_async_wait_all();")
