@@ -1,7 +1,7 @@
 """Distributed parity check: run plans over N processes (one GPU each, NCCL)
 and compare the gathered state with the CPU oracle.
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/dist_check.py [--quick] [--scale] [--qft34]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/dist_check.py [--quick] [--scale] [--qft34] [--qv34]
 """
 import gzip
 import json
@@ -86,7 +86,10 @@ def scale_checks(me, world):
         del res
     # mirror circuits U U^dagger over several GPUs (QV with 4-5 remaps, supremacy): every
     # amplitude must return to |0...0>, checked shard by shard
-    for name in ("mirror_qv30_h29-12", "mirror_qv31_h29-12", "mirror_sup31_h29-12", "mirror_qaoa31_h29-12"):
+    mirrors = ["mirror_qv30_h29-12", "mirror_qv31_h29-12", "mirror_sup31_h29-12", "mirror_qaoa31_h29-12"]
+    if "--qv34" in sys.argv:  # 34 qubits: 2 GPUs of 128 GiB each
+        mirrors.append("mirror_qv34_h33-12")
+    for name in mirrors:
         plan = planmod.load(str(ROOT / "plans" / f"{name}.json.gz"))
         if (1 << plan.g) < world:
             continue
