@@ -8,12 +8,17 @@ difference is where the state lives and how tasks execute:
 * the state is a complex128 CUDA tensor of shape (rows, 2^L); one process per
   GPU holds 2^g / world consecutive ranks as rows (all ranks on one GPU when
   not running distributed);
-* every ApplyFused task is compiled once (``program.py``) and runs as one
-  fused sweep kernel launch per tile group (``csrc/sweep.cu``);
-* Pack -> Exchange -> Unpack becomes an in-HBM bit swap for ranks on the
-  same GPU and a chunked NCCL exchange between GPUs (``comm.py``);
+* every ApplyFused task is compiled once (``program.py``, with a global
+  physical-layout planner) and runs as a few fused sweep kernels, generated
+  per sweep with NVRTC (``jit.py``) or interpreted for small states
+  (``csrc/sweep.cu``);
+* Pack -> Exchange -> Unpack is a relabel of layout bits for ranks on the
+  same GPU and, between GPUs, an in-place peer-memory swap over NVLink that
+  overlaps the sweeps around it (``comm.py``, ``csrc/peer.cu``; NCCL with
+  SVB200_REMAP=nccl);
 * the norm drift check is accumulated on the device inside the sweep and
-  validated once at the end of the run (same exception, same threshold).
+  validated once at the end of the run (same exception, same threshold);
+* sampling, compare and fidelity run on the device, shard by shard.
 
 There is no CPU execution path: without the CUDA library every call raises.
 """
