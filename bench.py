@@ -48,6 +48,7 @@ UNIT = "GB/s"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 E2E_HOST_BYTES = 48 << 30  # pinned host buffers per process (in and out each)
+TRAFFIC_REV = "r02"  # profiles/traffic.json entries measured on the current sweep code
 E2E_PIPELINE = os.environ.get("SVB200_E2E_PIPELINE", "1") != "0"  # two circuits in flight
 
 
@@ -225,6 +226,7 @@ def main() -> None:
     ap.add_argument("--workload", default="qft")
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sub-steps", type=int, default=6, help="steps of the N=1 sub-measurements (0: none)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -266,32 +268,56 @@ def main() -> None:
         del res
     barrier()
 
-    # timed region: K full circuits, device-timed with CUDA events
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    compute_s, launches, sweeps = 0.0, 0, 0
-    with ClockSampler(local) as clk:
+    def timed(plan_, steps, clk_=None):
+        """K full circuits, device-timed with CUDA events (max over ranks);
+        every sweep launch is bracketed by events on its stream as well."""
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        acc = {"compute_s": 0.0, "launches": 0, "sweeps": 0, "sweep_bytes": 0, "prof": {}}
+        executor.PROFILE_SWEEPS = True
         barrier()
         start.record()
-        for _ in range(args.steps):
-            res = run_plan(plan)
-            compute_s += res.stats.compute_seconds + res.stats.layout_seconds
-            launches += res.stats.kernel_launches
-            sweeps += res.stats.sweeps
-            stats = res.stats
-            del res
+        for _ in range(steps):
+            r = run_plan(plan_)
+            acc["compute_s"] += r.stats.compute_seconds + r.stats.layout_seconds
+            acc["launches"] += r.stats.kernel_launches
+            acc["sweeps"] += r.stats.sweeps
+            acc["sweep_bytes"] += r.stats.sweep_bytes
+            for di, lst in r.stats.sweep_profile.items():
+                acc["prof"].setdefault(di, []).extend(lst)
+            acc["stats"] = r.stats
+            del r
         stop.record()
         barrier()
-    elapsed = max_over_ranks(start.elapsed_time(stop) / 1e3)
-    compute_s = max_over_ranks(compute_s)
+        executor.PROFILE_SWEEPS = False
+        acc["elapsed"] = max_over_ranks(start.elapsed_time(stop) / 1e3)
+        acc["compute_s"] = max_over_ranks(acc["compute_s"])
+        return acc
+
+    with ClockSampler(local) as clk:
+        acc = timed(plan, args.steps)
+    elapsed, compute_s, launches, stats = acc["elapsed"], acc["compute_s"], acc["launches"], acc["stats"]
 
     total_bytes = plan_bytes(plan)
     value = total_bytes * args.steps / elapsed / 1e9
     peak, peak_kind = peak_hbm()
     rows = (1 << plan.g) // world
     fused = sum(1 for t in plan.tasks if t.kind == "ApplyFused")
-    launch_bytes = 32 * (rows << (plan.d - plan.g))  # one read + one write of the device state
-    sweeps = int(max_over_ranks(float(sweeps)))
-    achieved = launch_bytes * sweeps / compute_s / 1e9
+    sweeps = int(max_over_ranks(float(acc["sweeps"])))
+
+    def dominant(prof):
+        """The sweep kernel with the largest share of the step: its HBM bytes
+        per launch / its mean event-timed launch duration."""
+        best = max(prof.items(), key=lambda kv: sum(ms for _, ms in kv[1]))
+        di, lst = best
+        nb = sum(b for b, _ in lst) / len(lst)
+        ms = sum(t for _, t in lst) / len(lst)
+        share = sum(t for _, t in lst) / max(sum(t for l2 in prof.values() for _, t in l2), 1e-30)
+        return di, nb, ms, share
+
+    dom_di, dom_bytes, dom_ms, dom_share = dominant(acc["prof"])
+    dom_ms = max_over_ranks(dom_ms)
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    all_achieved = max_over_ranks(float(acc["sweep_bytes"])) / compute_s / 1e9
 
     # e2e: each process's initial rank blocks (|0...0> at layout phase 0) from
     # pinned host memory through run_plan(initial=...), final blocks back to
@@ -336,13 +362,44 @@ def main() -> None:
                              + ("" if nbuf == 2 else "; one pinned buffer per process, each step's output is the next input"),
                "ms_per_step": 1e3 * e2e_s}
 
+    # sub-measurements at N=1 (timed the same way, reported beside the headline):
+    # the same circuit with every sweep a full dense pass, and QV-30 (cfg3's
+    # family on one GPU), whose sweeps are FP64-heavy
+    subs = {}
+    if world == 1 and args.workload == "qft" and args.sub_steps > 0:
+        executor.SPARSE_START = False
+        for _ in range(3):
+            del_ = run_plan(plan)
+            del del_
+        a2 = timed(plan, args.sub_steps)
+        executor.SPARSE_START = True
+        subs["dense_passes"] = {
+            "note": "same plan, sparse start off: every sweep reads and writes the whole state",
+            "circuit_ms": 1e3 * a2["elapsed"] / args.sub_steps,
+            "value": total_bytes * args.sub_steps / a2["elapsed"] / 1e9,
+            "sweeps_frac": a2["sweep_bytes"] / a2["compute_s"] / 1e9 / peak}
+        qvp = load_plan("qv30_h30-12")
+        del_ = run_plan(qvp)
+        del del_
+        a3 = timed(qvp, max(1, args.sub_steps // 3))
+        k3 = max(1, args.sub_steps // 3)
+        di3, b3, ms3, sh3 = dominant(a3["prof"])
+        subs["qv30_h30-12"] = {
+            "circuit_ms": 1e3 * a3["elapsed"] / k3, "value": plan_bytes(qvp) * k3 / a3["elapsed"] / 1e9,
+            "sweeps_per_step": a3["sweeps"] // k3,
+            "sweeps_hbm_frac": a3["sweep_bytes"] / a3["compute_s"] / 1e9 / peak,
+            "dominant": {"sweep": di3, "launch_ms": ms3, "hbm_frac": b3 / (ms3 / 1e3) / 1e9 / peak,
+                         "share_of_sweep_time": sh3},
+            "compile_ms": 1e3 * a3["stats"].compile_seconds}
+
     traffic = fp64 = None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
             entry = json.loads(prof.read_text()).get(name) or {}
-            traffic = entry.get("bytes_per_launch")
-            fp64 = entry.get("fp64_pipe_pct")
+            if entry.get("rev") == TRAFFIC_REV and entry.get("sweep") == dom_di:  # same code, same kernel
+                traffic = entry.get("bytes_per_launch")
+                fp64 = entry.get("fp64_pipe_pct")
         except Exception:
             traffic = fp64 = None
 
@@ -354,17 +411,24 @@ def main() -> None:
                    "hierarchy": [plan.d - plan.g, 12], "apply_fused": fused,
                    "exchanges": [len(t.payload["swaps"]) for t in plan.tasks if t.kind == "Exchange"],
                    "parallelism": f"state-vector sharding over {n} GPU(s)",
-                   "l2": f"state {16 << plan.d >> 30} GiB >> 126 MB L2 (no flush needed)"},
+                   "l2": f"state {16 << plan.d >> 30} GiB >> 126 MB L2 (no flush needed)",
+                   "value_def": "SURVEY 8(d) algorithmic bytes, 32 B x 2^d per ApplyFused leaf, / circuit time: "
+                                "an effective rate comparable with the reference arm; the bytes the sweeps "
+                                "actually move are in roofline.all_sweeps"},
         "circuit_ms": 1e3 * elapsed / args.steps,
         "gates_per_s": sum(len(t.payload["gates"]) for t in plan.tasks if t.kind == "ApplyFused")
                         * args.steps / elapsed,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "sweep (NVRTC-specialised svb_jit_*; csrc/sweep.cu interpreter on small states)",
+                     "kernel": f"sweep {dom_di} (NVRTC-specialised svb_jit_*), the largest share of the step",
                      "peak_source": f"{peak_kind} hbm_gbs (copy bandwidth, burst)",
-                     "bytes_per_launch": launch_bytes,
-                     "launches_per_step": sweeps // args.steps,
-                     "launch_ms": 1e3 * compute_s / max(sweeps, 1),
+                     "bytes_per_launch": dom_bytes, "launch_ms": dom_ms, "share_of_sweep_time": dom_share,
+                     "bytes_note": "HBM bytes the launch must move: 16 B per amplitude read + 16 B per "
+                                   "amplitude written (sparse |0...0>-start sweeps read only the support)",
+                     "all_sweeps": {"achieved": all_achieved, "frac": all_achieved / peak,
+                                    "bytes_per_step": acc["sweep_bytes"] // args.steps,
+                                    "launches_per_step": sweeps // args.steps,
+                                    "sweep_ms_per_step": 1e3 * compute_s / args.steps},
                      "fp64_pipe_pct": fp64},
         "e2e": e2e,
         "gpu_launches": launches,
@@ -372,6 +436,8 @@ def main() -> None:
         "exchange_ms": 1e3 * stats.exchange_seconds,
         "clocks": clk.summary(),
     }
+    if subs:
+        line["sub"] = subs
     if world > 1:
         swap_s = max_over_ranks(stats.swap_seconds)
         line["nvlink"] = {

@@ -33,6 +33,17 @@ SVB_F void cp_async16(double2* smem_dst, const double2* gmem_src) {
   const u32 sa = (u32)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem_src) : "memory");
 }
+// zero-fill forms (src-size 0 reads no global memory; the address stays valid)
+SVB_F void cp_async16_zero(double2* smem_dst, const double2* any_gmem) {
+  const u32 sa = (u32)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;" ::"r"(sa), "l"(any_gmem) : "memory");
+}
+SVB_F void cp_async16_pred(double2* smem_dst, const double2* gmem_src, bool live, const double2* any_gmem) {
+  const u32 sa = (u32)__cvta_generic_to_shared(smem_dst);
+  const u32 n = live ? 16u : 0u;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(live ? gmem_src : any_gmem), "r"(n)
+               : "memory");
+}
 SVB_F void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 SVB_F void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 SVB_F void st_stream(double2* p, double2 v) {

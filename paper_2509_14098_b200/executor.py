@@ -65,6 +65,11 @@ class RunStats:
     layout_seconds: float = 0.0  # trailing sweeps restoring the reference layout
     swap_seconds: float = 0.0  # inter-GPU swap kernels alone (event-timed, no waits)
     nvlink_bytes: int = 0  # bytes this process sent over NVLink (= received)
+    # HBM bytes the sweep launches had to move (16 B per amplitude read or
+    # written; sparse sweeps of a |0...0> start move less, prog.sparse_bytes)
+    sweep_bytes: int = 0
+    # with executor.PROFILE_SWEEPS: descriptor -> [(bytes, ms)] per launch
+    sweep_profile: dict = field(default_factory=dict)
     trace: list = field(default_factory=list)  # (label, ms from run start) with SVB200_TRACE=1
 
 
@@ -113,6 +118,12 @@ def _dist_info(group=None):
     return 0, 1
 
 
+# runs from |0...0> compute only the support of the state until it covers
+# the device (program.sparse_start)
+SPARSE_START = os.environ.get("SVB200_SPARSE_START", "1") not in ("0", "false", "no")
+# per-launch CUDA events around every sweep (bench.py's roofline); off by default
+PROFILE_SWEEPS = False
+_prof_log: list | None = None  # (descriptor, bytes, start event, end event) of the current run
 JIT_MIN_D = int(os.environ.get("SVB200_JIT_MIN_D", "16"))
 # register slots per thread in generated kernels.  4 (256 threads x 16
 # amplitudes) needs one shared-memory round trip per 4 dense qubits instead of
@@ -142,8 +153,10 @@ class _Compiled:
     overlap: dict = field(default_factory=dict)  # descriptor -> overlapped exchange step
     cbits: dict = field(default_factory=dict)  # descriptor -> chunk bits its kernel was built with
     kernels: list | None = None  # per-descriptor JIT kernel handles (None: interpreter)
+    desc_bytes: list = field(default_factory=list)  # per descriptor: HBM bytes one full launch moves
     jit_seconds: float = 0.0
     zero_init: dict = field(default_factory=dict)  # descriptors that synthesise |0...0>
+    sparse: dict = field(default_factory=dict)  # descriptor -> (support, full_out), prog.sparse_start
     n_sweeps: int = 0
 
 
@@ -159,7 +172,7 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
 
     use_jit = _use_jit(geo, jit)
     key = (id(plan), len(plan.tasks), geo.d, geo.g, geo.h, geo.rank_base, str(device), use_jit,
-           zero_start)
+           zero_start, SPARSE_START)
     hit = _compile_cache.get(key)
     if hit is not None and hit[0] is plan:
         return hit[1]
@@ -191,19 +204,14 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
         from . import jit as jitmod
 
         t1 = time.perf_counter()
-        zinit = {}
-        if zero_start:
-            for st in dp.steps:
-                if st.kind == "exchange":
-                    break
-                if st.kind == "sweeps" and st.count:
-                    zinit[st.first] = 1 if geo.rank_base == 0 else 2
-                    break
-        names, cubins = jitmod.build_kernels(dp.buf, zero_init=zinit)
+        sparse = prog.sparse_start(dp, geo.D, geo.rank_base == 0) if (zero_start and SPARSE_START) else {}
+        names, cubins = jitmod.build_kernels(dp.buf, sparse=sparse)
         out.zero_init = dict(jitmod._LAST_ZERO_INIT)
+        out.sparse = sparse
         dev_index = device.index if device.index is not None else torch.cuda.current_device()
         out.kernels = [jitmod.load_kernel(n, c, dev_index) for n, c in zip(names, cubins)]
         out.jit_seconds = time.perf_counter() - t1
+    out.desc_bytes = [sum(prog.sparse_bytes(d, out.sparse.get(i))) for i, d in enumerate(dp.buf.descs)]
     _compile_cache.clear()  # keep one plan resident
     _compile_cache[key] = (plan, out)
     return out
@@ -461,6 +469,8 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
 
     stats = RunStats(task_counts={}, compute_seconds=0.0, exchange_seconds=0.0,
                      amps_moved=0, bytes_moved=0, exchanges=[])
+    global _prof_log
+    prof_log = _prof_log = [] if PROFILE_SWEEPS else None
 
     # protocol validation happens in task order, like the reference
     state: _State | None = None
@@ -552,6 +562,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 lib.svb_norm2(state.buf.data_ptr(), rows << L, norms[slot:].data_ptr(), stream)
                 launched = 1
             stats.sweeps += st.count
+            stats.sweep_bytes += sum(compiled.desc_bytes[st.first:st.first + st.count])
             stats.kernel_launches += launched
             fused_order.append(task.id)
         elif kind == "Pack":
@@ -607,6 +618,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
         e1.record()
         events.append(("Materialize", e0, e1))
         stats.sweeps += mat.count
+        stats.sweep_bytes += sum(compiled.desc_bytes[mat.first:mat.first + mat.count])
         stats.kernel_launches += launched
     fin_ev = torch.cuda.Event()
     fin_ev.record()
@@ -658,6 +670,8 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 stats.layout_seconds += sec
         for e0, e1 in swap_events:
             stats.swap_seconds += e0.elapsed_time(e1) / 1e3
+        for di, nb, e0, e1 in prof_log or ():
+            stats.sweep_profile.setdefault(di, []).append((nb, e0.elapsed_time(e1)))
         if norm_ev is not None:
             norm_ev.synchronize()
             vals = norm_host.numpy().copy()
@@ -756,11 +770,13 @@ def _launch_part(compiled, di, state, norms, grid_limit, stream, cbits, c) -> No
     fbits = [b for b in range(D) if b not in tin]
     val, tid = _part_values(cbits, c, fbits)
     ntiles = 1 << (D - K - len(cbits))
+    ev = _prof_begin()
     rc = lib.svb_jit_launch_sweep_part(compiled.kernels[di], state.buf.data_ptr(), compiled.blob.data_ptr(),
                                        compiled.descs[di:di + 1].ctypes.data,
                                        norms.data_ptr() if norms is not None else None,
                                        grid_limit, val, tid, ntiles, stream)
     _native.check(rc, "svb_jit_launch_sweep_part")
+    _prof_end(ev, di, compiled.desc_bytes[di] >> len(cbits) if compiled.desc_bytes else 0)
 
 
 def _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, stream, ovl) -> int:
@@ -843,6 +859,21 @@ def _remap_overlapped(state, xst, geo, group, ovl):
     return launches, e0, e1
 
 
+def _prof_begin():
+    if _prof_log is None:
+        return None
+    ev = torch.cuda.Event(enable_timing=True)
+    ev.record()
+    return ev
+
+
+def _prof_end(ev, di: int, nbytes: int) -> None:
+    if ev is not None:
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        _prof_log.append((di, nbytes, ev, e1))
+
+
 def _run_descs(compiled, first, count, state, rows_eff, L, norms, grid_limit, stream,
                skip=()) -> int:
     """Launch sweeps first .. first+count-1; returns the number of kernel launches."""
@@ -852,9 +883,11 @@ def _run_descs(compiled, first, count, state, rows_eff, L, norms, grid_limit, st
     descs = compiled.descs[first:first + count]
     nptr = norms.data_ptr() if norms is not None else None
     if compiled.kernels is None:
+        ev = _prof_begin()
         rc = lib.svb_run_sweeps(state.buf.data_ptr(), rows_eff, L, compiled.blob.data_ptr(),
                                 descs.ctypes.data, count, nptr, grid_limit, stream)
         _native.check(rc, "svb_run_sweeps")
+        _prof_end(ev, first, sum(compiled.desc_bytes[first:first + count]))
         return count
     launches = 0
     for i in range(count):
@@ -866,10 +899,12 @@ def _run_descs(compiled, first, count, state, rows_eff, L, norms, grid_limit, st
                 _launch_part(compiled, first + i, state, norms, grid_limit, stream, cb, c)
             launches += 1 << len(cb)
             continue
+        ev = _prof_begin()
         rc = lib.svb_jit_launch_sweep(compiled.kernels[first + i], state.buf.data_ptr(),
                                       compiled.blob.data_ptr(), descs[i:i + 1].ctypes.data, nptr,
                                       grid_limit, stream)
         _native.check(rc, "svb_jit_launch_sweep")
+        _prof_end(ev, first + i, compiled.desc_bytes[first + i])
         launches += 1
     return launches
 

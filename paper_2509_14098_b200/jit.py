@@ -107,12 +107,24 @@ def _xor_img(var: str, imgs) -> str:
 # kernel generator
 # ---------------------------------------------------------------------------
 
-def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int = 0) -> str:
+def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int = 0,
+                  sparse: tuple | None = None) -> str:
     """Straight-line kernel for one sweep.
 
     zero_init: 0 = load the state; 1 = the input is |0...0> with the unit
     amplitude on this device (synthesise tiles, no loads); 2 = the input is
-    all zeros on this device."""
+    all zeros on this device.
+
+    sparse = (support, full_out): the run started from |0...0> and only
+    amplitudes whose physical bits outside `support` are all 0 can be
+    nonzero (support None: every amplitude of this device is 0; see
+    program.sparse_start).  Only the tiles whose fixed bits lie inside the
+    support are computed ("live" tiles, enumerated compactly); their loads
+    of positions outside the support are zero-filled without touching
+    memory.  full_out: the next sweep reads the whole state, so every
+    position of a dead tile is written with zeros (coalesced streaming
+    stores, no loads, no arithmetic); otherwise dead tiles are not touched
+    (the next sweep never reads them)."""
     K, D = desc["K"], desc["D"]
     rb = int(desc.get("rb", prog.RB)) if hasattr(desc, "get") else int(desc["rb"])
     NR = 1 << rb
@@ -130,6 +142,26 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     fprime = [b for b in fbits if b not in cbits]
     fpos = {b: i for i, b in enumerate(fbits)}
     tb = K - rb  # thread bits
+    tinmask = sum(1 << b for b in tin)
+    ld_zero = 0  # tile bits whose loaded amplitudes are known zero (zero-filled)
+    NTV = "ntiles"  # tiles this launch enumerates
+    dead_slabs = []  # (fixed bit set to 1, free bits) covering the dead positions
+    if sparse is not None:
+        supp, full_out = sparse
+        assert not cbits, "sparse sweeps never run in parts"
+        if supp is None:
+            fprime = []
+            NTV = "0ll"
+            if full_out:
+                dead_slabs = [(None, list(range(D)))]
+        else:
+            fprime = [b for b in fbits if (supp >> b) & 1]
+            NTV = f"{1 << len(fprime)}ll"
+            ld_zero = tinmask & ~supp
+            if full_out:
+                zs = sorted((b for b in fbits if not (supp >> b) & 1), reverse=True)
+                for j, z in enumerate(zs):
+                    dead_slabs.append((z, [b for b in range(D) if b not in zs[:j + 1]]))
 
     L = []
     w = L.append
@@ -157,6 +189,8 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     w(f"  const u32 lds_t = {_xor_img('t', sw[:tb])};")
     w(f"  const u64 st_t = {_deposit('t', st_dev[:tb])};")
     w(f"  const u32 sts_t = {_xor_img('t', st_sw[:tb])};")
+    if ld_zero:
+        w(f"  const bool ld_live = (ld_t & {ld_zero}ull) == 0ull;")
     # per-thread phase tables do not depend on the tile: load them once
     for off in sorted({int(op["tab"]) for op in ops if op["kind"] != prog.OP_STAGE and int(op["tab"]) >= 0}):
         w(f"  const double2 tab{off} = __ldg(tab + {off} + t);")
@@ -188,6 +222,8 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
         return f"(({dep}) | part_val)" if cbits else dep
 
     def full_tid(var):  # index over all fixed bits (per-tile slot LUTs)
+        if sparse is not None:
+            return f"((long long)({_deposit(var, [fpos[b] for b in fprime])}))" if fprime else "0ll"
         if not cbits:
             return var
         return f"((long long)(({_deposit(var, [fpos[b] for b in fprime])}) | part_tid))"
@@ -216,7 +252,13 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                 if (it >> q) & 1:
                     dev |= 1 << tin[tb + q]
                     s ^= sw[tb + q]
-            w(f"      cp_async16({buf} + (lds_t ^ {s}u), state + ({base} | ld_t | {dev}ull));")
+            if dev & ld_zero:  # outside the support: zero, no memory access
+                w(f"      cp_async16_zero({buf} + (lds_t ^ {s}u), state);")
+            elif ld_zero:
+                w(f"      cp_async16_pred({buf} + (lds_t ^ {s}u), state + ({base} | ld_t | {dev}ull), "
+                  "ld_live, state);")
+            else:
+                w(f"      cp_async16({buf} + (lds_t ^ {s}u), state + ({base} | ld_t | {dev}ull));")
         if commit and items:
             w("      cp_async_commit();")
 
@@ -276,24 +318,24 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                 w("      }")
 
     if nct and nct <= NT and CTAB_AHEAD and not (zero_init and NO_AHEAD_ZERO):  # slots of this CTA's first tile
-        w("  if (tile_id < ntiles) {")
+        w(f"  if (tile_id < {NTV}) {{")
         w(f"    const u64 b0c = {origin('tile_id')};")
         emit_ctab("tile_id", "b0c", "ctab_base", per_thread=False)
         w("  }")
     if not zero_init:
-        w("  if (tile_id < ntiles) {")
+        w(f"  if (tile_id < {NTV}) {{")
         w(f"    const u64 b0 = {origin('tile_id')};")
         prefetch_items("smem", "b0", list(range(NR)))
         w("  }")
     w("  int iter = 0;")
-    w("  for (; tile_id < ntiles; ++iter, tile_id += gridDim.x) {")
+    w(f"  for (; tile_id < {NTV}; ++iter, tile_id += gridDim.x) {{")
     w("    const int r3 = iter % 3;")
     w(f"    double2* const tile = smem + r3 * {TILE};")
     w(f"    double2* const nbuf = smem + (r3 == 2 ? 0 : r3 + 1) * {TILE};")
     w(f"    double2* const pbuf = smem + (r3 == 0 ? 2 : r3 - 1) * {TILE};")
     w(f"    const u64 base = {origin('tile_id')};")
     w(f"    double2* const ctab = ctab_base + (iter & 1) * {max(nct, 1)};")
-    w("    const bool has_next = tile_id + gridDim.x < ntiles;")
+    w(f"    const bool has_next = tile_id + gridDim.x < {NTV};")
     w("    const long long nx = tile_id + gridDim.x;")
     w(f"    const u64 bn = {origin('nx')};")
     w("    const long long px = tile_id - gridDim.x;")
@@ -461,6 +503,14 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     store_items("pbuf", "bp", list(range(NR)))
     w("  }")
     w("  cp_async_wait_all();")
+    for z, free in dead_slabs:  # dead positions of a sparse sweep: zeros
+        n = 1 << len(free)
+        one = f" | {1 << z}ull" if z is not None else ""
+        w("  {")
+        w(f"    const long long gs = (long long)gridDim.x * {NT};")
+        w(f"    for (long long c = (long long)blockIdx.x * {NT} + t; c < {n}ll; c += gs)")
+        w(f"      st_stream(state + (({_deposit('c', free)}){one}), make_double2(0.0, 0.0));")
+        w("  }")
     w("  if (norm_out != nullptr) {")
     full = "0xffffffffu" if NT >= 32 else f"{(1 << NT) - 1}u"
     for o in (16, 8, 4, 2, 1):
@@ -662,22 +712,29 @@ def _compile(src: str, name: str) -> bytes:
 
 
 def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: int | None = None,
-                  zero_init: dict | None = None):
+                  zero_init: dict | None = None, sparse: dict | None = None):
     """Generate + compile one kernel per sweep descriptor; returns (names, cubins).
 
     zero_init maps descriptor index -> 1/2 for sweeps whose input is known to
-    be |0...0> (see kernel_source); _LAST_ZERO_INIT records which were used."""
+    be |0...0> (see kernel_source); _LAST_ZERO_INIT records which were used.
+    sparse maps descriptor index -> (support, full_out) from
+    program.sparse_start (a run from |0...0>); it implies zero_init for the
+    sweeps that start from the unit vector or from zeros."""
     srcs, names = [], []
-    zero_init = zero_init or {}
+    zero_init = dict(zero_init or {})
+    sparse = dict(sparse or {})
+    for i, (supp, _) in sparse.items():
+        if supp is None or supp == 0:
+            zero_init[i] = 2 if supp is None else 1
     used = {}
     for i, d in enumerate(buf.descs):
         ops = buf.ops[d["op_begin"]: d["op_begin"] + d["op_count"]]
         zi = zero_init.get(i, 0)
-        if zi and not any(int(o["kind"]) == prog.OP_STAGE for o in ops):
-            zi = 0  # no register stage to synthesise into
+        if zi and not (zi == 2 and i in sparse) and not any(int(o["kind"]) == prog.OP_STAGE for o in ops):
+            raise ValueError(f"sweep {i} cannot synthesise |0...0> (no register stage)")
         if zi:
             used[i] = zi
-        body = kernel_source("KNAME", d, ops, buf.coef, zi)
+        body = kernel_source("KNAME", d, ops, buf.coef, zi, sparse.get(i))
         h = hashlib.sha1(body.encode()).hexdigest()[:16]
         name = f"{prefix}_{h}"
         srcs.append(body.replace("KNAME", name))

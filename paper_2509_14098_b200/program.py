@@ -887,6 +887,71 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
     return DeviceProgram(buf=buf, steps=steps, init_perm=init, n_fused=slot)
 
 
+def sparse_start(dp: "DeviceProgram", D: int, unit: bool) -> dict:
+    """Support of the state along the sweeps of a run that starts from |0...0>.
+
+    A sweep changes amplitudes only along its tile bits, and its store
+    permutes the tile bits among themselves, so from |0...0> the amplitudes
+    that can be nonzero are those whose physical bits outside a support set
+    S are 0, with S growing by each sweep's tile bits (S starts empty with
+    the unit amplitude at index 0 of the device holding it, or None on the
+    devices that hold only zeros).  Returns {descriptor: (S_in, full_out)}
+    for the leading sweeps whose S_in is not the whole device: they compute
+    only the tiles inside the support (jit.kernel_source) and the last one
+    also writes the zeros outside it (full_out), after which the state is
+    fully materialised.  The sequence ends at the first remap that moves
+    data, at a sweep that runs in parts around an overlapped remap, or when
+    the support covers every bit.  The first sweep must have a register
+    stage to synthesise the unit vector; otherwise no sweep is sparse."""
+    full = (1 << D) - 1
+    supp = 0 if unit else None
+    seq = []
+    stop = False
+    for st in dp.steps:
+        if stop:
+            break
+        if st.kind == "exchange":
+            if st.swaps:
+                break
+            continue  # a relabel: no data moves
+        for i in range(st.first, st.first + st.count):
+            d = dp.buf.descs[i]
+            if d.get("cbits") or (supp is not None and supp == full):
+                stop = True
+                break
+            seq.append((i, supp))
+            if supp is not None:
+                tin = [int(b) for b in d["tin"][:d["K"]]]
+                assert sorted(tin) == sorted(int(b) for b in d["st_dev"][:d["K"]]), "store leaves the tile"
+                supp |= sum(1 << b for b in tin)
+    if not seq:
+        return {}
+    i0, s0 = seq[0]
+    d0 = dp.buf.descs[i0]
+    ops = dp.buf.ops[d0["op_begin"]: d0["op_begin"] + d0["op_count"]]
+    if s0 == 0 and not any(int(o["kind"]) == OP_STAGE for o in ops):
+        return {}
+    return {i: (s, k == len(seq) - 1) for k, (i, s) in enumerate(seq)}
+
+
+def sparse_bytes(desc: dict, sparse) -> tuple:
+    """(bytes read, bytes written) of one sweep launch: 16 B per amplitude;
+    a sparse sweep reads only the support and writes only live tiles (plus
+    every dead position when full_out)."""
+    K, D = int(desc["K"]), int(desc["D"])
+    if sparse is None:
+        return 16 << D, 16 << D
+    supp, full_out = sparse
+    if supp is None:
+        return 0, (16 << D) if full_out else 0
+    tinm = sum(1 << int(b) for b in desc["tin"][:K])
+    nsupp = bin(supp).count("1")
+    nlive_fixed = bin(supp & ~tinm).count("1")
+    rd = 0 if supp == 0 else 16 << nsupp
+    wr = (16 << D) if full_out else 16 << (nlive_fixed + K)
+    return rd, wr
+
+
 def _independent3(vs) -> bool:
     a, b, c = vs
     return all(x != 0 for x in (a, b, c, a ^ b, a ^ c, b ^ c, a ^ b ^ c))

@@ -181,6 +181,56 @@ def make_cfg1(out: Path) -> None:
     np.savez_compressed(out / "cfg1_fp.npz", **fps)
 
 
+# Benchmark-family plans whose sweeps run at real tile geometry (D > K = 12):
+# fixed-bit predicates, per-tile slot tables and multi-row devices are then
+# exercised against the reference itself.  (name, qasm generator, budgets,
+# initial basis state or None)
+FAMILY_CASES = [
+    ("qv20_h18-12", lambda: workloads.quantum_volume(20, seed=20), [18, 12], None),
+    ("qv22_h22-12", lambda: workloads.quantum_volume(22, seed=22), [22, 12], None),
+    ("qv21_h20-12", lambda: workloads.quantum_volume(21, seed=21, depth=10), [20, 12], None),
+    ("qaoa20_h18-12", lambda: workloads.qaoa_maxcut(20, seed=20, p=2), [18, 12], None),
+    ("sup20_h19-12", lambda: workloads.random_supremacy(20, seed=20, depth=12), [19, 12], None),
+    ("qft20_h19-12_x", lambda: workloads.qft(20), [19, 12], 0xB5A3D),
+    ("qv20_h20-12_x", lambda: workloads.quantum_volume(20, seed=23, depth=8), [20, 12], 0x3C0F1),
+]
+FP_SAMPLES = 8192
+
+
+def fingerprint(flat: np.ndarray, seed: int) -> dict:
+    """Sampled amplitudes + weighted sums of the flat rank-block storage: a
+    permutation of the storage changes them (the tests recompute them)."""
+    rng = np.random.default_rng(seed)
+    n = flat.size
+    idx = np.sort(rng.choice(n, size=min(FP_SAMPLES, n), replace=False))
+    w = np.exp(2j * np.pi * rng.random(n))
+    return {"idx": idx, "amps": flat[idx], "sum": np.array([flat.sum()]),
+            "wsum": np.array([(w * flat).sum()]), "norm": np.array([np.vdot(flat, flat).real])}
+
+
+def make_families(out: Path) -> None:
+    docs, fps = {}, {}
+    for name, gen, budgets, x in FAMILY_CASES:
+        src = gen()
+        plan = plan_of(src, budgets)
+        initial = None
+        if x is not None:
+            initial = np.zeros(1 << plan.d, dtype=np.complex128)
+            initial[x] = 1.0
+        t0 = time.perf_counter()
+        res = run_plan(plan, initial=initial)
+        dt = time.perf_counter() - t0
+        docs[name] = {"plan": json.loads(to_json(plan)), "stats": stats_doc(res), "seconds": dt,
+                      "initial_basis": x, "budgets": budgets, "fp_seed": len(docs) + 1}
+        flat = np.asarray(res.state.blocks).reshape(-1)
+        for k, v in fingerprint(flat, seed=len(docs)).items():
+            fps[f"{name}::{k}"] = v
+        print(f"family {name}: d={plan.d} g={plan.g} reference run_plan {dt:.1f} s", flush=True)
+    with gzip.open(out / "families.json.gz", "wt") as fh:
+        json.dump(docs, fh)
+    np.savez_compressed(out / "families_fp.npz", **fps)
+
+
 BENCH = [
     ("qft30_h30-12", lambda: workloads.qft(30), [30, 12]),
     ("qft31_h30-12", lambda: workloads.qft(31), [30, 12]),
@@ -247,10 +297,15 @@ if __name__ == "__main__":
     ap.add_argument("--plans", action="store_true", help="also write benchmark plans to plans/")
     ap.add_argument("--only-plans", action="store_true")
     ap.add_argument("--force", action="store_true", help="regenerate existing plans")
+    ap.add_argument("--families", action="store_true", help="only the benchmark-family fingerprints")
     a = ap.parse_args()
+    if a.families:
+        make_families(HERE)
+        sys.exit(0)
     if not a.only_plans:
         (HERE / "gates.json").write_text(json.dumps(gates_doc(), indent=1, sort_keys=True) + "\n")
         make_grid(HERE)
         make_cfg1(HERE)
+        make_families(HERE)
     if a.plans or a.only_plans:
         make_plans(ROOT / "plans", a.force)

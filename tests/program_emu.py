@@ -30,11 +30,17 @@ def _xor_img(vals: np.ndarray, imgs) -> np.ndarray:
     return out
 
 
-def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None) -> None:
-    """In-place on the flat device state (length 2^D)."""
+def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None, sparse=None) -> None:
+    """In-place on the flat device state (length 2^D).
+
+    sparse: per descriptor (support, full_out) or None (program.sparse_start);
+    a sparse sweep computes only live tiles, zero-fills loads outside the
+    support (the unit vector when the support is empty) and writes zeros
+    over the dead tiles only when full_out, as the generated kernel does."""
     ops_all, coef, tab, cterms, cofs_all = (parts[k] for k in ("ops", "coef", "tab", "cterms", "cofs"))
     cofs_base = 0
-    for d in descs:
+    for di, d in enumerate(descs):
+        sp = sparse[di] if sparse is not None else None
         K, D = int(d["K"]), int(d["D"])
         RB = int(d["rb"])
         NR = 1 << RB
@@ -61,6 +67,12 @@ def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None)
             for i, b in enumerate(fbits):
                 if (tile_id >> i) & 1:
                     base |= 1 << b
+            if sp is not None:
+                supp, full_out = sp
+                if supp is None or base & ~supp:  # dead tile
+                    if full_out:
+                        state[base | ld_dev] = 0.0
+                    continue
             ctab = np.ones(max(nct, 1), dtype=np.complex128)
             for i in range(nct):
                 for q in range(int(cofs[i]), int(cofs[i + 1])):
@@ -68,7 +80,13 @@ def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None)
                     if (base & int(ct["mask"])) == int(ct["mask"]):
                         ctab[i] *= complex(ct["re"], ct["im"])
             tile = np.empty(1 << K, dtype=np.complex128)
-            tile[ld_s] = state[base | ld_dev]
+            if sp is None:
+                tile[ld_s] = state[base | ld_dev]
+            elif sp[0] == 0:  # synthesised |0...0>
+                tile[ld_s] = np.where((base | ld_dev) == 0, 1.0 + 0j, 0j)
+            else:  # zero-filled outside the support
+                pos = base | ld_dev
+                tile[ld_s] = np.where((pos & ~sp[0]) == 0, state[pos], 0j)
             x = None
             J = None
             dev_base = None
@@ -184,7 +202,8 @@ def _devmap(jt: np.ndarray, tin) -> np.ndarray:
     return out
 
 
-def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog.RB, stable: bool = False):
+def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog.RB, stable: bool = False,
+                 sparse: bool = False, kmax: int = prog.KMAX):
     """Run a plan through the compiled device programs of `world` devices.
 
     Each device gets its own program (plan_device with its rank range);
@@ -199,7 +218,7 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
     progs, parts = [], []
     for w in range(world):
         geo = prog.DeviceGeometry(d=d, g=g, h=h, rank_base=w * rows, pad_to=prog.RB)
-        dp = prog.plan_device(plan, geo, rb=rb, stable_threads=stable)
+        dp = prog.plan_device(plan, geo, rb=rb, stable_threads=stable, kmax=kmax)
         blob, descs, p = prog.pack(dp.buf)
         progs.append((geo, dp, descs, p))
     D = progs[0][0].D
@@ -210,6 +229,12 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
                 [(s.kind, s.task_id, s.swaps) for s in progs[0][1].steps]
     states = [np.zeros(1 << D, dtype=np.complex128) for _ in range(world)]
     states[0][0] = 1.0
+    sp_of = []  # per device: descriptor -> (support, full_out)
+    for w, (geo, dp, descs, p) in enumerate(progs):
+        sp = prog.sparse_start(dp, D, w == 0) if sparse else {}
+        if sp:  # unwritten memory: any read outside the support would poison the result
+            states[w][:] = np.nan
+        sp_of.append(sp)
     norms = np.zeros(max(progs[0][1].n_fused, 1))
     steps = {s.task_id: s for s in progs[0][1].steps}
     for task in plan.tasks:
@@ -218,7 +243,8 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
             slot = sum(1 for t in plan.tasks[: plan.tasks.index(task)] if t.kind == "ApplyFused")
             for w, (geo, dp, descs, p) in enumerate(progs):
                 sw = {s.task_id: s for s in dp.steps}[task.id]
-                run_sweeps(states[w], descs[sw.first: sw.first + sw.count], p, norms)
+                run_sweeps(states[w], descs[sw.first: sw.first + sw.count], p, norms,
+                           [sp_of[w].get(i) for i in range(sw.first, sw.first + sw.count)])
             if st.count == 0:
                 norms[slot] = norms[slot - 1] if slot else sum(float(np.sum(np.abs(s) ** 2)) for s in states)
         elif task.kind == "Exchange":
@@ -235,6 +261,7 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
     mat = steps.get(None)
     if mat is not None:
         for w, (geo, dp, descs, p) in enumerate(progs):
-            run_sweeps(states[w], descs[mat.first: mat.first + mat.count], p, None)
+            run_sweeps(states[w], descs[mat.first: mat.first + mat.count], p, None,
+                       [sp_of[w].get(i) for i in range(mat.first, mat.first + mat.count)])
     blocks = np.concatenate([s[: rows << L] for s in states]).reshape(nr, 1 << L)
     return blocks, norms

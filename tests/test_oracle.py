@@ -77,3 +77,16 @@ def test_dense_simulate_matches_reference(grid_docs, grid_states):
         assert orc.compare(ref, grid_states[doc["name"] + "::dense"]) < 1e-10, doc["name"]
         n += 1
     assert n > 100
+
+
+@pytest.mark.parametrize("name", ["qaoa20_h18-12", "sup20_h19-12", "qft20_h19-12_x"])
+def test_oracle_family_fingerprints(family_docs, family_fp, name):
+    """The oracle on benchmark-family plans at 20 qubits against the reference's fingerprints."""
+    from conftest import check_fingerprint, family_initial
+
+    doc = family_docs[name]
+    plan = plan_from_doc(doc["plan"])
+    blocks, st = orc.run_plan(plan, backend="c", nthreads=4, initial=family_initial(doc))
+    assert st["task_counts"] == doc["stats"]["task_counts"]
+    assert st["exchanges"] == doc["stats"]["exchanges"]
+    check_fingerprint(blocks.reshape(-1), family_fp, name, doc["fp_seed"], tol=1e-12)

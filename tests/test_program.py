@@ -31,6 +31,29 @@ def test_single_device_programs_match_reference(grid_docs, grid_states, rb, stab
     print("worst", worst)
 
 
+@pytest.mark.parametrize("world,kmax", [(1, 12), (1, 6), (1, 7), (2, 6), (4, 7)])
+def test_sparse_start_programs_match_reference(grid_docs, grid_states, world, kmax):
+    """Runs from |0...0> computing only the support (program.sparse_start):
+    unwritten memory starts as NaN, so a read outside the support shows.
+    Small tiles (kmax < D) give several sparse sweeps with dead tiles."""
+    from paper_2509_14098_b200 import program as prog
+
+    n = multi = 0
+    for doc in _cases(grid_docs, grid_states, min_ranks=world):
+        plan = plan_from_doc(doc["plan"])
+        blocks, norms = program_emu.emulate_plan(plan, world=world, sparse=True, kmax=kmax)
+        geo = prog.DeviceGeometry(d=plan.d, g=plan.g, h=plan.g - (world.bit_length() - 1), rank_base=0,
+                                  pad_to=prog.RB)
+        multi += len(prog.sparse_start(prog.plan_device(plan, geo, kmax=kmax), geo.D, True)) > 1
+        err = float(np.max(np.abs(blocks - grid_states[doc["name"]])))
+        assert err < TOL, (doc["name"], world, err)
+        if world == 1:
+            assert np.all(np.abs(norms - 1) < 1e-8), doc["name"]
+        n += 1
+    assert n > 50
+    assert multi > (20 if kmax < 12 else -1)
+
+
 @pytest.mark.parametrize("world", [2, 4])
 def test_multi_device_programs_match_reference(grid_docs, grid_states, world):
     n = 0
