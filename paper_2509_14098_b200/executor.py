@@ -154,6 +154,7 @@ class _Compiled:
     cbits: dict = field(default_factory=dict)  # descriptor -> chunk bits its kernel was built with
     kernels: list | None = None  # per-descriptor JIT kernel handles (None: interpreter)
     desc_bytes: list = field(default_factory=list)  # per descriptor: HBM bytes one full launch moves
+    norm_alias: dict = field(default_factory=dict)  # slot -> slot whose sweep measured its norm
     jit_seconds: float = 0.0
     zero_init: dict = field(default_factory=dict)  # descriptors that synthesise |0...0>
     sparse: dict = field(default_factory=dict)  # descriptor -> (support, full_out), prog.sparse_start
@@ -198,6 +199,7 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
             overlap.setdefault(st.chain[0], {})["chain"] = st
     out = _Compiled(dev_blob, descs, steps, dp.init_perm, dp.n_fused, time.perf_counter() - t0,
                     host, n_sweeps=len(dp.buf.descs))
+    out.norm_alias = dict(dp.norm_alias)
     out.overlap = overlap if use_jit else {}
     out.cbits = {i: d["cbits"] for i, d in enumerate(dp.buf.descs) if d.get("cbits")} if use_jit else {}
     if use_jit and dp.buf.descs:
@@ -500,7 +502,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 dist.all_reduce(t, group=group)
                 vals = t.cpu().numpy()
         for slot, tid in enumerate(fused_order):
-            nv = float(vals[slot])
+            nv = float(vals[compiled.norm_alias.get(slot, slot)])
             if abs(nv - 1.0) > DRIFT_TOL:
                 raise NonUnitaryDrift(f"norm drifted to {nv!r}")
 
@@ -554,6 +556,8 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 launched = _run_descs(compiled, st.first, st.count, state, rows_eff, L, norms, grid_limit,
                                       stream)
                 _mark(f"sweeps{st.first}-{st.first + st.count - 1} end")
+            elif slot in compiled.norm_alias:  # merged into a sweep of another leaf
+                pass
             elif slot > 0:  # relabel-only leaf: the state (and its norm) is unchanged
                 norms[slot:slot + 1].copy_(norms[slot - 1:slot])
             elif initial is None:  # |0...0> (possibly not materialised yet) has norm 1

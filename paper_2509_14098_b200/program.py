@@ -556,6 +556,11 @@ class DeviceProgram:
     steps: list
     init_perm: list  # reference device bit -> physical device bit at Alloc
     n_fused: int
+    # ApplyFused slot -> slot whose sweep measured its norm (itself, a later
+    # slot when leaves share a sweep, an earlier one after trailing
+    # relabels); slots absent here precede every sweep and carry the
+    # initial norm
+    norm_alias: dict = field(default_factory=dict)
 
 
 class _Lookahead:
@@ -637,6 +642,8 @@ def _pad_displaced(tile: set, where: list, look: _Lookahead, K: int, L: int) -> 
             tile |= add
 
 
+# sweeps may span consecutive ApplyFused leaves (plan_device.run_segment)
+MERGE_LEAVES = os.environ.get("SVB200_MERGE_LEAVES", "1") not in ("0", "false", "no")
 MAX_CHAIN = int(os.environ.get("SVB200_MAX_CHAIN", "3"))  # sweeps before a remap run depth-first with it
 # chunk bits and swapped bits of an overlapped remap stay at or above this
 # physical bit: the bulk-copy swap moves contiguous runs of 2^bit amplitudes
@@ -767,42 +774,57 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
             init[r] = d0[where[r]]
     where = list(init)
 
-    slot = 0
-    leaf_iter = iter(leaves)
-    task_leaf = {tid: prims for tid, prims in leaves}
+    task_leaf = dict(leaves)
+    norm_alias: dict = {}
+    last_measured = -1  # slot of the latest sweep-measured norm
+    task_slot = {}
     for task in plan.tasks:
-        if task.kind == "Exchange":
-            sw = []
-            for s in task.payload["swaps"]:
-                ib = geo.g - 1 - s["rank_bit"]
-                lb = L - 1 - s["local_bit"]
-                if ib < geo.h:  # executor.py:224-281 moves data between rows of this
-                    # device: here only the labels of the two bits swap
-                    where[L + ib], where[lb] = where[lb], where[L + ib]
-                else:
-                    sw.append((ib, where[lb]))
-            steps.append(Step("exchange", task.id, swaps=sw))
-            continue
-        if task.kind != "ApplyFused":
-            continue
-        prims = task_leaf[task.id]
-        base = leaf_start[task.id]
-        first = len(buf.descs)
-        i = 0
+        if task.kind == "ApplyFused":
+            task_slot[task.id] = len(task_slot)
+
+    def run_segment(seg: list) -> None:
+        """Sweeps for a run of consecutive ApplyFused tasks (no remap between
+        them).  With MERGE_LEAVES a sweep may span several leaves: gates of
+        consecutive leaves share a tile whenever their qubits fit, so the
+        many small leaves the partitioner emits (one to three gates on one
+        or two qubits) cost no memory pass of their own.  Each sweep is
+        launched by the task it ends in; a leaf that ends inside a sweep
+        takes that sweep's norm (gates are unitary: the norm after the
+        sweep is the norm after the leaf, up to rounding)."""
+        nonlocal last_measured
+        prims, owner, ends = [], [], []
+        for ti, task in enumerate(seg):
+            ps = task_leaf[task.id]
+            prims.extend(ps)
+            owner.extend([ti] * len(ps))
+            ends.append(len(prims))
         n = len(prims)
-        if all(isinstance(pr, Swap) for pr in prims):
-            # a pure relabeling: no data moves, the norm is unchanged
-            for pr in prims:
-                where[pr.a], where[pr.b] = where[pr.b], where[pr.a]
-            steps.append(Step("sweeps", task.id, first, 0))
-            slot += 1
-            continue
-        while True:
+        base = leaf_start[seg[0].id]
+        firsts = {ti: None for ti in range(len(seg))}
+        counts = {ti: 0 for ti in range(len(seg))}
+        completed = 0  # tasks [0, completed) are done
+        i = 0
+        # tasks with no primitives before the first sweep carry the previous norm
+        while completed < len(seg) and ends[completed] == 0:
+            completed += 1
+        while i < n:
+            limit = n if MERGE_LEAVES else ends[owner[i]]
+            if all(isinstance(pr, Swap) for pr in prims[i:limit]):
+                # relabels only (the rest of the segment, or a SWAP-only
+                # leaf when leaves are not merged): no data moves
+                for pr in prims[i:limit]:
+                    where[pr.a], where[pr.b] = where[pr.b], where[pr.a]
+                i = limit
+                while completed < len(seg) and ends[completed] <= i:
+                    if last_measured >= 0:
+                        norm_alias[task_slot[seg[completed].id]] = last_measured
+                    completed += 1
+                continue
             # greedy extent of this sweep under the current layout
             trial = list(where)
             need = set(range(low))
             j = i
-            while j < n:
+            while j < limit:
                 pr = prims[j]
                 if isinstance(pr, Swap):
                     trial[pr.a], trial[pr.b] = trial[pr.b], trial[pr.a]
@@ -842,13 +864,48 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
             for p in tile:
                 if p in inv:
                     where[inv[p]] = dest[p]
-            sp.norm_slot = slot if j >= n else -1
+            done = []
+            while completed < len(seg) and ends[completed] <= j:
+                done.append(task_slot[seg[completed].id])
+                completed += 1
+            sp.norm_slot = done[-1] if done else -1
+            for sl in done:
+                norm_alias[sl] = done[-1]
+            if done:
+                last_measured = done[-1]
+            at = owner[j - 1]  # launched by the task this sweep ends in
+            if firsts[at] is None:
+                firsts[at] = len(buf.descs)
+            counts[at] += 1
             emit_sweep(sp, geo, buf, rb, stable_threads)
             i = j
-            if i >= n:
-                break
-        steps.append(Step("sweeps", task.id, first, len(buf.descs) - first))
-        slot += 1
+        for ti, task in enumerate(seg):
+            f = firsts[ti] if firsts[ti] is not None else len(buf.descs)
+            steps.append(Step("sweeps", task.id, f, counts[ti]))
+
+    seg: list = []
+    for task in plan.tasks:
+        if task.kind == "ApplyFused":
+            seg.append(task)
+            continue
+        if task.kind != "Exchange":
+            continue
+        if seg:
+            run_segment(seg)
+            seg = []
+        sw = []
+        for s in task.payload["swaps"]:
+            ib = geo.g - 1 - s["rank_bit"]
+            lb = L - 1 - s["local_bit"]
+            if ib < geo.h:  # executor.py:224-281 moves data between rows of this
+                # device: here only the labels of the two bits swap
+                where[L + ib], where[lb] = where[lb], where[L + ib]
+            else:
+                sw.append((ib, where[lb]))
+        steps.append(Step("exchange", task.id, swaps=sw))
+    if seg:
+        run_segment(seg)
+    slot = len(task_slot)
 
     _plan_overlap(steps, buf, geo, overlap_bits)
 
@@ -884,7 +941,7 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
         emit_sweep(sp, geo, buf, rb, stable_threads)
     if passes:
         steps.append(Step("materialize", None, first, passes))
-    return DeviceProgram(buf=buf, steps=steps, init_perm=init, n_fused=slot)
+    return DeviceProgram(buf=buf, steps=steps, init_perm=init, n_fused=slot, norm_alias=norm_alias)
 
 
 def sparse_start(dp: "DeviceProgram", D: int, unit: bool) -> dict:

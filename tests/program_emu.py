@@ -245,8 +245,8 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
                 sw = {s.task_id: s for s in dp.steps}[task.id]
                 run_sweeps(states[w], descs[sw.first: sw.first + sw.count], p, norms,
                            [sp_of[w].get(i) for i in range(sw.first, sw.first + sw.count)])
-            if st.count == 0:
-                norms[slot] = norms[slot - 1] if slot else sum(float(np.sum(np.abs(s) ** 2)) for s in states)
+            if st.count == 0 and slot not in progs[0][1].norm_alias:
+                norms[slot] = norms[slot - 1] if slot else 1.0  # |0...0> (maybe not materialised yet)
         elif task.kind == "Exchange":
             # global index = device * 2^(L+h) + row * 2^L + local
             full = np.concatenate([s[: rows << L] for s in states])
@@ -264,4 +264,6 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
             run_sweeps(states[w], descs[mat.first: mat.first + mat.count], p, None,
                        [sp_of[w].get(i) for i in range(mat.first, mat.first + mat.count)])
     blocks = np.concatenate([s[: rows << L] for s in states]).reshape(nr, 1 << L)
+    alias = progs[0][1].norm_alias
+    norms = np.array([norms[alias.get(i, i)] for i in range(len(norms))])
     return blocks, norms

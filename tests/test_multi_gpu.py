@@ -36,3 +36,24 @@ def test_dist_parity(world, remap):
     tail = (r.stdout + r.stderr)[-3000:]
     assert r.returncode == 0, tail
     assert "0 mismatches" in r.stdout, tail
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_dist_parity_colocated(world):
+    """The inter-process remap on a one-GPU box: `world` processes share
+    cuda:0 (gloo control plane), map each other's state with CUDA IPC and
+    swap through the same bulk-copy kernel, flag epochs and overlapped
+    chunks as across GPUs; checked against the goldens, the oracle, the
+    closed-form QFT and mirrors, plus sharded compare/fidelity/sampling."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    env = dict(os.environ, SVB200_REMAP="peer")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "tools" / "dist_check.py"),
+           "--quick", "--scale", "--colocate"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
+    tail = (r.stdout + r.stderr)[-3000:]
+    assert r.returncode == 0, tail
+    assert "0 mismatches" in r.stdout, tail
+    print(r.stdout[-2000:])

@@ -2,6 +2,10 @@
 and compare the gathered state with the CPU oracle.
 
     torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/dist_check.py [--quick] [--scale] [--qft34] [--qv34]
+                                                                             [--colocate]
+
+--colocate runs every process on cuda:0 with a gloo control plane (the
+inter-process peer remap then runs between processes sharing one GPU).
 """
 import gzip
 import json
@@ -151,8 +155,16 @@ def scale_checks(me, world):
 
 def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if "--colocate" in sys.argv:
+        # every process on cuda:0 (the driver's GPU test box has one GPU):
+        # the peer-memory remap still maps the other processes' state with
+        # CUDA IPC and orders the swaps with flag words; NCCL refuses two
+        # ranks on one device, so the control plane is gloo
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     world = dist.get_world_size()
     me = dist.get_rank()
     docs = json.load(gzip.open(ROOT / "tests/golden/grid.json.gz", "rt"))
