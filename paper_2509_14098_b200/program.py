@@ -346,7 +346,7 @@ def _bits_of(pr) -> set:
     return set()
 
 
-def fuse_prims(prims: list) -> list:
+def fuse_prims(prims: list, owners: list | None = None):
     """Merge runs of gates confined to one qubit pair into a single 4x4 (e.g.
     the u,u,cx,u,u,cx,u,u,cx,u,u form of an SU(4)).
 
@@ -355,13 +355,28 @@ def fuse_prims(prims: list) -> list:
     dense gates; otherwise its gates are emitted unchanged (phases and bit
     flips are cheaper than a 4x4).  The decision depends only on gate
     structure, never on device-specific constants.
+
+    A fused block takes the place of its last gate: primitives between its
+    gates touch other bits (one touching its pair would have closed it) and
+    commute with it, so later sweeps see the gates near their original
+    position.
+
+    owners (optional): a tag per primitive (non-decreasing); then returns
+    (prims, tags) where a fused primitive carries the tag of its last gate.
     """
-    out: list = []
-    blocks: list = []  # open blocks: dict(bits=set, prims=list)
+    placed: list = []  # (input position, primitive, tag)
+    blocks: list = []  # open blocks: dict(bits=set, prims=list, own=list, pos=list)
+    tagged = owners is not None
+    owners = owners if tagged else [0] * len(prims)
 
     def close(blk):
         blocks.remove(blk)
         ps = blk["prims"]
+        top = blk["own"][-1]
+        at = blk["pos"][-1]
+
+        def emit(pr, o, k=None):
+            placed.append((at if k is None else k, pr, o))
         dense = [p for p in ps if isinstance(p, Dense1)]
         nonperm = [p for p in dense if not p.perm]
         bits = sorted(blk["bits"])
@@ -370,7 +385,7 @@ def fuse_prims(prims: list) -> list:
             m = np.eye(4, dtype=np.complex128)
             for p in ps:
                 m = _embed2(p, a, b) @ m
-            out.append(Dense2(a, b, m))
+            emit(Dense2(a, b, m), top)
         elif len(nonperm) >= 2 and len(bits) == 1 and all(not p.ctrl for p in dense):
             (x,) = bits
             m = np.eye(2, dtype=np.complex128)
@@ -380,27 +395,43 @@ def fuse_prims(prims: list) -> list:
                 else:
                     g = np.eye(2, dtype=np.complex128) if p.noop else p.m
                 m = g @ m
-            out.append(Dense1(x, m, {}))
+            emit(Dense1(x, m, {}), top)
         else:
-            out.extend(ps)
+            for p, o, k in zip(ps, blk["own"], blk["pos"]):
+                emit(p, o, k)
 
-    for pr in prims:
+    for k, (pr, o) in enumerate(zip(prims, owners)):
         bits = _bits_of(pr)
         fusable = isinstance(pr, (Dense1, Factor)) and len(bits) <= 2 and bits
         hit = [blk for blk in blocks if blk["bits"] & bits]
+        if fusable and len(hit) > 1 and len(set().union(bits, *(b["bits"] for b in hit))) <= 2:
+            # single-qubit blocks on the two bits of this gate (e.g. the u, u
+            # before the first cx of an SU(4)) commute and join one block
+            items = sorted((kk, pp, oo) for b in hit for kk, pp, oo in zip(b["pos"], b["prims"], b["own"]))
+            for b in hit[1:]:
+                blocks.remove(b)
+            hit = hit[:1]
+            hit[0]["bits"] = set().union(*(b["bits"] for b in hit), *(_bits_of(pp) for _, pp, _ in items))
+            hit[0]["pos"] = [kk for kk, _, _ in items]
+            hit[0]["prims"] = [pp for _, pp, _ in items]
+            hit[0]["own"] = [oo for _, _, oo in items]
         if fusable and len(hit) == 1 and len(hit[0]["bits"] | bits) <= 2:
             hit[0]["bits"] |= bits
             hit[0]["prims"].append(pr)
+            hit[0]["own"].append(o)
+            hit[0]["pos"].append(k)
             continue
         for blk in hit:
             close(blk)
         if fusable and (isinstance(pr, Dense1) or len(bits) == 2):
-            blocks.append({"bits": set(bits), "prims": [pr]})
+            blocks.append({"bits": set(bits), "prims": [pr], "own": [o], "pos": [k]})
         else:
-            out.append(pr)
+            placed.append((k, pr, o))
     for blk in list(blocks):
         close(blk)
-    return out
+    placed.sort(key=lambda x: x[0])
+    out = [pr for _, pr, _ in placed]
+    return (out, [o for _, _, o in placed]) if tagged else out
 
 
 def build_sweep(prims: list, tile: list, where: list) -> SweepProgram:
@@ -733,21 +764,48 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
     L, D = geo.L, geo.D
     K = min(kmax, D)
     low = min(low, K)
-    leaves = []
+    raw = {}
     for task in plan.tasks:
         if task.kind == "ApplyFused":
             layout = plan.layout_phases[task.payload["phase"]]
             prims = []
             for e in task.payload["gates"]:
                 prims.extend(resolve_entry(e, layout, geo))
-            leaves.append((task.id, fuse_prims(prims) if fuse else prims))
-    # planning stream: every leaf's primitives, with a marker per remap
-    stream, leaf_start = [], {}
-    prims_of = dict(leaves)
+            raw[task.id] = prims
+    # segments: runs of ApplyFused tasks with no remap between them.  With
+    # MERGE_LEAVES the gate fusion runs over a whole segment (an SU(4) split
+    # between two leaves is fused again); each fused primitive belongs to the
+    # latest task it contains a gate of
+    segs, cur = [], []
     for task in plan.tasks:
         if task.kind == "ApplyFused":
-            leaf_start[task.id] = len(stream)
-            stream.extend(prims_of[task.id])
+            cur.append(task)
+        elif task.kind == "Exchange" and cur:
+            segs.append(cur)
+            cur = []
+    if cur:
+        segs.append(cur)
+    seg_prims = {}  # first task id -> (prims, owners)
+    for seg in segs:
+        prims, owners = [], []
+        if MERGE_LEAVES and fuse:
+            for ti, task in enumerate(seg):
+                prims.extend(raw[task.id])
+                owners.extend([ti] * len(raw[task.id]))
+            prims, owners = fuse_prims(prims, owners)
+        else:
+            for ti, task in enumerate(seg):
+                ps = fuse_prims(raw[task.id]) if fuse else raw[task.id]
+                prims.extend(ps)
+                owners.extend([ti] * len(ps))
+        seg_prims[seg[0].id] = (prims, owners)
+    # planning stream: every segment's primitives, with a marker per remap
+    stream, leaf_start = [], {}
+    for task in plan.tasks:
+        if task.kind == "ApplyFused":
+            if task.id in seg_prims:
+                leaf_start[task.id] = len(stream)
+                stream.extend(seg_prims[task.id][0])
         elif task.kind == "Exchange":
             remote_bits = []
             for s in task.payload["swaps"]:
@@ -774,7 +832,6 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
             init[r] = d0[where[r]]
     where = list(init)
 
-    task_leaf = dict(leaves)
     norm_alias: dict = {}
     last_measured = -1  # slot of the latest sweep-measured norm
     task_slot = {}
@@ -792,12 +849,16 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
         takes that sweep's norm (gates are unitary: the norm after the
         sweep is the norm after the leaf, up to rounding)."""
         nonlocal last_measured
-        prims, owner, ends = [], [], []
-        for ti, task in enumerate(seg):
-            ps = task_leaf[task.id]
-            prims.extend(ps)
-            owner.extend([ti] * len(ps))
-            ends.append(len(prims))
+        prims, owner = seg_prims[seg[0].id]
+        # task t is complete once every primitive owned by tasks <= t is
+        # emitted: ends[t] = 1 + last such position
+        last = {}
+        for k, o in enumerate(owner):
+            last[o] = k + 1
+        ends, e = [], 0
+        for ti in range(len(seg)):
+            e = max(e, last.get(ti, 0))
+            ends.append(e)
         n = len(prims)
         base = leaf_start[seg[0].id]
         firsts = {ti: None for ti in range(len(seg))}
@@ -808,7 +869,7 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
         while completed < len(seg) and ends[completed] == 0:
             completed += 1
         while i < n:
-            limit = n if MERGE_LEAVES else ends[owner[i]]
+            limit = n if MERGE_LEAVES else min(e for e in ends if e > i)
             if all(isinstance(pr, Swap) for pr in prims[i:limit]):
                 # relabels only (the rest of the segment, or a SWAP-only
                 # leaf when leaves are not merged): no data moves
@@ -873,7 +934,7 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
                 norm_alias[sl] = done[-1]
             if done:
                 last_measured = done[-1]
-            at = owner[j - 1]  # launched by the task this sweep ends in
+            at = min(t for t, e in enumerate(ends) if e >= j)  # launched by the task it ends in
             if firsts[at] is None:
                 firsts[at] = len(buf.descs)
             counts[at] += 1
