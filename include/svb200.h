@@ -265,6 +265,10 @@ int svb_peer_swap_bulk(svb_c128* local, void* const* peers, int npeers, int64_t 
  *   earlier work of the stream; or hold the stream until *addr >= value. */
 int svb_stream_write_u32(void* addr, uint32_t value, void* stream);
 int svb_stream_wait_u32(void* addr, uint32_t value, void* stream);
+/* svb_stream_create: a non-blocking CUDA stream on the current device for
+ *   one purpose (uploads, downloads, overlapped remap chunks); never freed.
+ *   Dedicated handles never alias each other or torch's pooled streams. */
+int svb_stream_create(void** stream);
 /* svb_copy: n-amplitude SM copy; either pointer may be a mapped peer's. */
 int svb_copy(svb_c128* dst, const svb_c128* src, int64_t n, int grid_limit, void* stream);
 int svb_peer_swap(svb_c128* local, void* const* peers, int npeers, int64_t rows, int L,

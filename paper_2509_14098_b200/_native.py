@@ -61,6 +61,7 @@ _SIGS = {
                            _int),
     "svb_stream_write_u32": ([_vp, _u32, _vp], _int),
     "svb_stream_wait_u32": ([_vp, _u32, _vp], _int),
+    "svb_stream_create": ([_c.POINTER(_vp)], _int),
     "svb_copy": ([_vp, _vp, _i64, _int, _vp], _int),
     "svb_peer_swap": ([_vp, _vp, _int, _i64, _int, _pi32, _int, _vp, _vp, _vp, _vp, _int, _int, _vp], _int),
 }

@@ -184,7 +184,7 @@ PEER_MODE = os.environ.get("SVB200_REMAP", "peer")  # "peer" | "nccl"
 # bulk swap geometry: 148 one-warp CTAs with 3 x 2 x 4 KiB stages (24.7 KB of
 # shared memory, 48 registers) fit on every SM beside a running sweep CTA and
 # still reach ~690 GB/s per direction (tools/p2p_bench.py, round 1)
-SWAP_GRID = int(os.environ.get("SVB200_SWAP_GRID", "148"))
+SWAP_GRID = int(os.environ.get("SVB200_SWAP_GRID", "0"))  # 0: one CTA per SM
 SWAP_PIECE = int(os.environ.get("SVB200_SWAP_PIECE", "4096"))
 SWAP_STAGES = int(os.environ.get("SVB200_SWAP_STAGES", "3"))
 SWAP_AHEAD = int(os.environ.get("SVB200_SWAP_AHEAD", "1"))
@@ -258,6 +258,11 @@ class PeerContext:
 
     @staticmethod
     def _off(kind: int, src: int, chunk: int) -> int:
+        # the words live in the peers' allocations: an index past the table
+        # would write into their state
+        if not (0 <= src < FLAG_RANKS and 0 <= chunk < FLAG_CHUNKS and kind in (READY, DONE)):
+            raise ValueError(f"flag word out of range (kind {kind}, rank {src}, chunk {chunk}): "
+                             f"at most {FLAG_RANKS} processes and {FLAG_CHUNKS} chunks")
         return 4 * ((kind * FLAG_RANKS + src) * FLAG_CHUNKS + chunk)
 
     def signal(self, kind, chunk, ranks, epoch, stream) -> None:
@@ -343,6 +348,8 @@ def symmetric_buffer(n: int, device, group):
         arena.last_use = None
     buf = torch.as_tensor(_Lease(arena, n), device=device)
     me, world = dist.get_rank(group), dist.get_world_size(group)
+    if world > FLAG_RANKS:
+        raise ValueError(f"peer-memory remap supports at most {FLAG_RANKS} processes (got {world})")
     rec = np.frombuffer(arena.handle + int(arena.epoch).to_bytes(8, "little"), dtype=np.uint8)
     mine = torch.from_numpy(rec.copy()).to(device)
     allr = [torch.empty_like(mine) for _ in range(world)]
@@ -444,7 +451,8 @@ def peer_exchange(state, remote: list, ctx: PeerContext, stream, epoch: int, cbi
     e0.record(es)
     run = 16 << min([lb for _, lb in remote] + list(cbits or []))  # bytes per contiguous run
     if run >= MIN_BULK_RUN:
-        _native.check(lib.svb_peer_swap_bulk(*args, SWAP_GRID, SWAP_PIECE, SWAP_STAGES, SWAP_AHEAD, stream),
+        grid = SWAP_GRID or torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        _native.check(lib.svb_peer_swap_bulk(*args, grid, SWAP_PIECE, SWAP_STAGES, SWAP_AHEAD, stream),
                       "svb_peer_swap_bulk")
     else:  # short runs: 16-byte register loads/stores from every SM
         _native.check(lib.svb_peer_swap(*args, 0, 0, stream), "svb_peer_swap")

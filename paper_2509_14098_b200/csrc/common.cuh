@@ -21,7 +21,9 @@ int cuda_status(cudaError_t e, const char* what);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-constexpr int kNumSMs = 148;
+// SM count of the current device (cached per device): grids are sized in
+// multiples of it (persistent kernels: one CTA per SM)
+int num_sms();
 
 // ---- complex128 arithmetic on double2 ------------------------------------
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {

@@ -23,6 +23,18 @@ int cuda_status(cudaError_t e, const char* what) {
   return SVB_ECUDA;
 }
 
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
 namespace {
 
 struct GateGeom {
@@ -152,7 +164,7 @@ __global__ void k_diag(double2* __restrict__ blocks, uint64_t total, GateGeom g,
 
 int grid_for(uint64_t work, int threads) {
   uint64_t b = (work + threads - 1) / threads;
-  uint64_t cap = (uint64_t)kNumSMs * 16;
+  uint64_t cap = (uint64_t)num_sms() * 16;
   if (b > cap) b = cap;
   return b ? (int)b : 1;
 }
@@ -200,7 +212,7 @@ extern "C" int svb_apply_gate(svb_c128* blocks, int64_t ranks, int64_t n, const 
     case 2: k_gate_small<2><<<grid_for(groups, 256), 256, 0, st>>>(b, L, groups, g, matrix); break;
     case 3: k_gate_small<3><<<grid_for(groups, 256), 256, 0, st>>>(b, L, groups, g, matrix); break;
     default: {
-      int blocks_n = (int)(groups < (uint64_t)kNumSMs * 32 ? groups : (uint64_t)kNumSMs * 32);
+      int blocks_n = (int)(groups < (uint64_t)num_sms() * 32 ? groups : (uint64_t)num_sms() * 32);
       size_t smem = sizeof(double2) << p;
       k_gate_wide<<<blocks_n, 1 << p, smem, st>>>(b, L, groups, g, matrix);
     }

@@ -139,7 +139,7 @@ extern "C" int svb_jit_launch_sweep_part(void* kernel, svb_c128* state, const vo
   double* nrm = (norm_out && d.norm_slot >= 0) ? norm_out + d.norm_slot : nullptr;
   long long nt = ntiles;
   void* args[] = {&st, &tab, &ct, &cofs, &nrm, &part_val, &part_tid, &nt};
-  int64_t grid = kNumSMs;
+  int64_t grid = num_sms();
   if (grid_limit > 0 && grid > grid_limit) grid = grid_limit;
   if (grid > ntiles) grid = ntiles;
   if (grid <= 0) return SVB_OK;

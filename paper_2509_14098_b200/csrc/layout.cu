@@ -103,7 +103,7 @@ __global__ void k_bitperm(const double2* __restrict__ src, double2* __restrict__
 
 int grid_for(uint64_t work, int threads) {
   uint64_t b = (work + threads - 1) / threads;
-  const uint64_t cap = (uint64_t)kNumSMs * 32;
+  const uint64_t cap = (uint64_t)num_sms() * 32;
   if (b > cap) b = cap;
   return b ? (int)b : 1;
 }

@@ -360,7 +360,7 @@ extern "C" int svb_copy(svb_c128* dst, const svb_c128* src, int64_t n, int grid_
   }
   if (n == 0) return SVB_OK;
   int64_t gx = (n + 4 * 256 - 1) / (4 * 256);
-  const int64_t cap = grid_limit > 0 ? grid_limit : (int64_t)kNumSMs * 8;
+  const int64_t cap = grid_limit > 0 ? grid_limit : (int64_t)num_sms() * 8;
   if (gx > cap) gx = cap;
   k_copy<<<(unsigned)gx, 256, 0, as_stream(stream)>>>(reinterpret_cast<double2*>(dst),
                                                       reinterpret_cast<const double2*>(src), n);
@@ -423,7 +423,7 @@ extern "C" int svb_peer_swap(svb_c128* local, void* const* peers, int npeers, in
     }
   if (maxn == 0) return SVB_OK;
   int64_t gx = (maxn + 4 * block - 1) / (4 * block);
-  const int64_t cap = grid_limit > 0 ? grid_limit : (int64_t)kNumSMs * 2048 / block;
+  const int64_t cap = grid_limit > 0 ? grid_limit : (int64_t)num_sms() * 2048 / block;
   if (gx > cap) gx = cap;
   k_peer_swap<<<dim3((unsigned)gx, (unsigned)npeers), block, 0, as_stream(stream)>>>(a);
   SVB_CHECK_LAUNCH("svb_peer_swap");
@@ -479,5 +479,13 @@ extern "C" int svb_stream_wait_u32(void* addr, uint32_t value, void* stream) {
     set_error("cuStreamWaitValue32 failed (%d)", r);
     return SVB_ECUDA;
   }
+  return SVB_OK;
+}
+
+extern "C" int svb_stream_create(void** stream) {
+  cudaStream_t s;
+  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return cuda_status(e, "cudaStreamCreateWithFlags");
+  *stream = reinterpret_cast<void*>(s);
   return SVB_OK;
 }

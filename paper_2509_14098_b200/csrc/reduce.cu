@@ -24,11 +24,18 @@ struct WI {
   int64_t i;
 };
 
-// larger weight wins; ties go to the smaller index (numpy argmax = first)
+// larger weight wins; ties go to the smaller index (numpy argmax = first).
+// NaN is the largest weight, as in numpy's argmax: a NaN amplitude makes the
+// phase and the result NaN (executor.py:361-372 then fails `compare < tol`)
 __device__ __forceinline__ WI better(WI a, WI b) {
+  const bool an = a.w != a.w, bn = b.w != b.w;
+  if (an || bn) return (an && bn) ? (b.i < a.i ? b : a) : (bn ? b : a);
   if (b.w > a.w || (b.w == a.w && b.i < a.i)) return b;
   return a;
 }
+
+// max that keeps a NaN (numpy's max propagates it; fmax would drop it)
+__device__ __forceinline__ double nmax(double m, double v) { return (v > m || v != v) ? v : m; }
 
 __device__ __forceinline__ double cabs_(double2 z) { return hypot(z.x, z.y); }
 
@@ -82,13 +89,13 @@ __global__ void k_maxdev(const double2* __restrict__ a, const double2* __restric
     const double2 bi = b[i], ai = a[i];
     const double2 pb = make_double2(__dsub_rn(__dmul_rn(phi.x, bi.x), __dmul_rn(phi.y, bi.y)),
                                     __dadd_rn(__dmul_rn(phi.x, bi.y), __dmul_rn(phi.y, bi.x)));
-    m = fmax(m, cabs_(make_double2(__dsub_rn(ai.x, pb.x), __dsub_rn(ai.y, pb.y))));
+    m = nmax(m, cabs_(make_double2(__dsub_rn(ai.x, pb.x), __dsub_rn(ai.y, pb.y))));
   }
   __shared__ double shm[kThreads];
   shm[threadIdx.x] = m;
   __syncthreads();
   for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) shm[threadIdx.x] = fmax(shm[threadIdx.x], shm[threadIdx.x + o]);
+    if (threadIdx.x < o) shm[threadIdx.x] = nmax(shm[threadIdx.x], shm[threadIdx.x + o]);
     __syncthreads();
   }
   if (threadIdx.x == 0) dpart[blockIdx.x] = shm[0];
@@ -97,11 +104,11 @@ __global__ void k_maxdev(const double2* __restrict__ a, const double2* __restric
 __global__ void k_max_final(const double* dpart, int nparts, double* out) {
   __shared__ double shm[kThreads];
   double m = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += blockDim.x) m = fmax(m, dpart[i]);
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) m = nmax(m, dpart[i]);
   shm[threadIdx.x] = m;
   __syncthreads();
   for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) shm[threadIdx.x] = fmax(shm[threadIdx.x], shm[threadIdx.x + o]);
+    if (threadIdx.x < o) shm[threadIdx.x] = nmax(shm[threadIdx.x], shm[threadIdx.x + o]);
     __syncthreads();
   }
   if (threadIdx.x == 0) out[0] = shm[0];
@@ -123,6 +130,8 @@ struct WI2 {
 };
 
 __device__ __forceinline__ WI2 better2(WI2 a, WI2 b) {
+  const bool an = a.w != a.w, bn = b.w != b.w;
+  if (an || bn) return (an && bn) ? (b.bi < a.bi ? b : a) : (bn ? b : a);
   if (b.w > a.w || (b.w == a.w && b.bi < a.bi)) return b;
   return a;
 }
@@ -180,13 +189,13 @@ __global__ void k_maxdev_phi(const double2* __restrict__ a, const double2* __res
     const double2 bi = b[i], ai = a[i];
     const double2 pb = make_double2(__dsub_rn(__dmul_rn(phi.x, bi.x), __dmul_rn(phi.y, bi.y)),
                                     __dadd_rn(__dmul_rn(phi.x, bi.y), __dmul_rn(phi.y, bi.x)));
-    m = fmax(m, cabs_(make_double2(__dsub_rn(ai.x, pb.x), __dsub_rn(ai.y, pb.y))));
+    m = nmax(m, cabs_(make_double2(__dsub_rn(ai.x, pb.x), __dsub_rn(ai.y, pb.y))));
   }
   __shared__ double shm[kThreads];
   shm[threadIdx.x] = m;
   __syncthreads();
   for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) shm[threadIdx.x] = fmax(shm[threadIdx.x], shm[threadIdx.x + o]);
+    if (threadIdx.x < o) shm[threadIdx.x] = nmax(shm[threadIdx.x], shm[threadIdx.x + o]);
     __syncthreads();
   }
   if (threadIdx.x == 0) dpart[blockIdx.x] = shm[0];
@@ -194,7 +203,7 @@ __global__ void k_maxdev_phi(const double2* __restrict__ a, const double2* __res
 
 int nblocks(int64_t n) {
   int64_t b = (n + kThreads - 1) / kThreads;
-  if (b > kNumSMs * 8) b = kNumSMs * 8;
+  if (b > num_sms() * 8) b = num_sms() * 8;
   return b > 0 ? (int)b : 1;
 }
 

@@ -101,7 +101,7 @@ extern "C" int svb_probs_sorted(const svb_c128* shard, int D, const int32_t* per
     }
   const uint64_t n = uint64_t(1) << D;
   uint64_t blocks = (n + 255) / 256;
-  if (blocks > (uint64_t)kNumSMs * 16) blocks = (uint64_t)kNumSMs * 16;
+  if (blocks > (uint64_t)num_sms() * 16) blocks = (uint64_t)num_sms() * 16;
   k_probs_sorted<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(reinterpret_cast<const double2*>(shard), n,
                                                                    sp, out);
   SVB_CHECK_LAUNCH("svb_probs_sorted");
@@ -125,7 +125,7 @@ extern "C" int svb_sample_prefix(const double* cdf, int d, uint64_t fixed_mask, 
     if (p < d && !((fixed_mask >> p) & 1)) ++below;
   }
   int64_t blocks = (nshots + 255) / 256;
-  if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
   k_sample_prefix<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(cdf, mid, nshots, a, out);
   SVB_CHECK_LAUNCH("svb_sample_prefix");
   return SVB_OK;

@@ -437,7 +437,7 @@ int launch_sweep(double2* state, const SweepArgs& a, int grid_limit, cudaStream_
     attr_set = true;
   }
   const int64_t ntiles = int64_t(1) << (a.d.D - K);
-  int64_t grid = kNumSMs;
+  int64_t grid = num_sms();
   if (grid_limit > 0 && grid > grid_limit) grid = grid_limit;
   if (grid > ntiles) grid = ntiles;
   k_sweep<<<(unsigned)grid, 1 << (K - RB), smem, st>>>(state, a);

@@ -97,6 +97,36 @@ class RunResult:
 # ---------------------------------------------------------------------------
 
 
+def _arg_device(x):
+    """CUDA device of a DistState / tensor argument (None otherwise)."""
+    if isinstance(x, DistState):
+        x = x.blocks
+    if isinstance(x, torch.Tensor) and x.device.type == "cuda":
+        return x.device
+    return None
+
+
+def _on_device(pick):
+    """Run the wrapped entry point with its CUDA device current: kernels,
+    events, torch streams and JIT attributes bind to the current device, so
+    a device= argument (or a state on another GPU) must be made current."""
+    import functools
+
+    def deco(fn):
+        @functools.wraps(fn)
+        def wrapper(*args, **kw):
+            dev = pick(*args, **kw)
+            if dev is None:
+                return fn(*args, **kw)
+            dev = torch.device(dev)
+            if dev.type != "cuda":
+                return fn(*args, **kw)
+            with torch.cuda.device(dev):
+                return fn(*args, **kw)
+        return wrapper
+    return deco
+
+
 def _stream_ptr(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
@@ -405,7 +435,7 @@ class _State:
 def _upload_stream(device):
     up = _UPLOAD_STREAMS.get(device)
     if up is None:
-        up = _UPLOAD_STREAMS[device] = torch.cuda.Stream(device=device)
+        up = _side_stream(_UPLOAD_STREAMS, device)
     return up
 
 
@@ -421,6 +451,25 @@ def _pinned_host(x) -> bool:
 
 
 _COPY_STREAMS: dict = {}  # device -> stream of run_plan(out=...) downloads
+_COMM_STREAMS: dict = {}  # device -> stream of overlapped remap chunks
+
+
+def _side_stream(cache: dict, device) -> torch.cuda.Stream:
+    """A dedicated stream per device and purpose, created once: torch's
+    pooled streams (torch.cuda.Stream()) are handed out round-robin from 32
+    per device, so a fresh one per run would eventually alias the upload,
+    copy or NCCL stream and serialise behind it.  Native handles never alias."""
+    st = cache.get(device)
+    if st is None:
+        from . import _native
+        import ctypes
+
+        lib = _native.load()
+        h = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _native.check(lib.svb_stream_create(ctypes.byref(h)), "svb_stream_create")
+        st = cache[device] = torch.cuda.ExternalStream(h.value, device=device)
+    return st
 _UPLOAD_STREAMS: dict = {}  # device -> stream of pinned initial-state uploads
 _FENCE: dict = {}  # device -> one-element tensor (see run_plan(out=...))
 _META_STREAMS: dict = {}  # device -> stream of the deferred drift-check read (run_plan(wait=False))
@@ -434,6 +483,7 @@ def _pinned_take(n: int) -> torch.Tensor:
     return torch.empty(max(n, 4096), dtype=torch.float64, pin_memory=True)
 
 
+@_on_device(lambda plan, *a, device=None, **k: device)
 def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=None, *,
              device=None, group=None, grid_limit: int = 0, jit=None, out=None,
              wait: bool = True) -> RunResult:
@@ -644,7 +694,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
         src_ev.record()
         ms = _META_STREAMS.get(device)
         if ms is None:
-            ms = _META_STREAMS[device] = torch.cuda.Stream(device=device)
+            ms = _side_stream(_META_STREAMS, device)
         ms.wait_event(src_ev)
         norm_host = _pinned_take(nsum.numel())  # pooled: a fresh pinned allocation syncs the device
         with torch.cuda.stream(ms):
@@ -704,7 +754,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             raise DimensionMismatch(f"out {tuple(out.shape)} {out.dtype} != ({rows}, 2^{L}) complex128")
         cs = _COPY_STREAMS.get(device)
         if cs is None:
-            cs = _COPY_STREAMS[device] = torch.cuda.Stream(device=device)
+            cs = _side_stream(_COPY_STREAMS, device)
         # The drift check's small device-to-host read was the last operation on
         # this stream; the stream's next operation would then wait behind the
         # download below in the copy-engine queue (measured, tools/copy_overlap.py).
@@ -746,9 +796,10 @@ def _overlap_bits() -> int:
     from . import comm
 
     env = os.environ.get("SVB200_OVERLAP_BITS")
-    if env is not None:
-        return int(env)
-    return 3 if comm.PEER_MODE == "peer" else 0
+    bits = int(env) if env is not None else (3 if comm.PEER_MODE == "peer" else 0)
+    if (1 << bits) > comm.FLAG_CHUNKS:  # one flag word per chunk and partner
+        raise ValueError(f"SVB200_OVERLAP_BITS={bits}: at most {comm.FLAG_CHUNKS.bit_length() - 1} chunk bits")
+    return bits
 
 
 OVERLAP_GRID = int(os.environ.get("SVB200_OVERLAP_GRID", "0"))  # 0: every SM
@@ -836,7 +887,7 @@ def _remap_overlapped(state, xst, geo, group, ovl):
     from . import comm
 
     if ovl["comm"] is None:
-        ovl["comm"] = torch.cuda.Stream()
+        ovl["comm"] = _side_stream(_COMM_STREAMS, torch.device("cuda", torch.cuda.current_device()))
     cs = ovl["comm"]
     remote = [(ib - geo.h, lb) for ib, lb in xst.swaps]
     pre_evs = ovl["pre"].pop(id(xst))
@@ -966,6 +1017,7 @@ def _all_blocks(state: DistState) -> torch.Tensor:
     return torch.cat(parts, dim=0)
 
 
+@_on_device(lambda state, *a, **k: _arg_device(state))
 def gather_device(state: DistState) -> torch.Tensor:
     """Dense qubit-0-most-significant vector on the device (executor.py:320-326)."""
     blocks = _all_blocks(state)
@@ -984,6 +1036,7 @@ def gather(state: DistState) -> np.ndarray:
     return gather_device(state).cpu().numpy()
 
 
+@_on_device(lambda dense, plan, phase=0, device=None, **k: device or _arg_device(dense))
 def scatter(dense, plan, phase: int = 0, device=None, local_perm=None) -> DistState:
     """Distribute a dense state into rank blocks at the given layout phase (executor.py:329-343).
 
@@ -1055,9 +1108,11 @@ def _compare_sharded(a: DistState, b: DistState) -> float:
     for t in parts:
         w = float(t[0].item())
         bi = int(t[1:2].view(torch.int64).item())
-        if best is None or w > best[0] or (w == best[0] and bi < best[1]):
+        if best is None or w > best[0] or (w == best[0] and bi < best[1]) or (w != w and best[0] == best[0]):
             best = (w, bi, complex(float(t[2].item()), float(t[3].item())))
     w, _, z = best
+    if w != w:  # a NaN amplitude: numpy's argmax picks it and the result is NaN
+        return float("nan")
     phi = z / abs(z) if w > 0.0 else 1.0 + 0.0j
     dev = torch.zeros(1, dtype=torch.float64, device=device)
     _native.check(lib.svb_shard_maxdev(A.data_ptr(), B.data_ptr(), n, phi.real, phi.imag, dev.data_ptr(),
@@ -1066,6 +1121,7 @@ def _compare_sharded(a: DistState, b: DistState) -> float:
     return float(dev.item())
 
 
+@_on_device(lambda a, b, device=None: device or _arg_device(a) or _arg_device(b))
 def compare(a, b, device=None) -> float:
     """Max amplitude deviation after aligning global phase at the largest amplitude.
 
@@ -1090,6 +1146,7 @@ def compare(a, b, device=None) -> float:
     return float(out.item())
 
 
+@_on_device(lambda a, b, device=None: device or _arg_device(a) or _arg_device(b))
 def fidelity(a, b, device=None) -> float:
     """|<a|b>|^2 / (<a|a><b|b>) on the device (sharded DistStates: per shard, then all-reduced)."""
     if _same_sharding(a, b):
@@ -1111,6 +1168,7 @@ def fidelity(a, b, device=None) -> float:
     return float((ov.abs() ** 2 / (torch.vdot(A, A).real * torch.vdot(B, B).real)).item())
 
 
+@_on_device(lambda dense, shots, seed, device=None: device or _arg_device(dense))
 def sample(dense, shots: int, seed: int | None, device=None) -> dict:
     """Seeded measurement histogram {bitstring: count}, qubit 0 first
     (executor.py:375-383), computed on the GPU by ``sampling.sample_state``:
@@ -1133,6 +1191,7 @@ def sample(dense, shots: int, seed: int | None, device=None) -> dict:
     return sampling.sample_state(st, shots, seed)
 
 
+@_on_device(lambda circuit, device=None: device)
 def oracle_simulate(circuit, device=None) -> np.ndarray:
     """Dense reference-order simulation from |0...0>, on the GPU (executor.py:346-358)."""
     from . import kernels

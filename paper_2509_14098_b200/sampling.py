@@ -79,6 +79,13 @@ def sample_state(state, shots: int, seed: int | None) -> dict:
         return t
 
     stream = torch.cuda.current_stream(device).cuda_stream
+    need = 8 << D  # |a|^2 of the shard, float64
+    free, _ = torch.cuda.mem_get_info(device)
+    if need + (1 << 30) > free + torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device):
+        from .errors import TooLarge
+
+        raise TooLarge(f"sampling needs {need >> 30} GiB of probabilities beside the state on {device} "
+                       f"({free >> 30} GiB free): run on more GPUs or sample a gathered sub-state")
     probs = torch.empty(1 << D, dtype=torch.float64, device=device)
     arr, p32 = _native.i32_array(perm)
     _native.check(lib.svb_probs_sorted(blocks.contiguous().data_ptr(), D, p32, probs.data_ptr(), stream),

@@ -221,3 +221,23 @@ def test_deferred_finish_pipelining_and_drift():
         r.wait()
     with pytest.raises(ValueError):
         run_plan(plan, shots=10, wait=False)
+
+
+def test_compare_propagates_nan():
+    """numpy's argmax/max return NaN for a NaN amplitude, so the reference's
+    compare() is NaN (and `compare(...) < tol` fails); the device reduction
+    must not drop it (fmax would)."""
+    import math
+
+    from oracle import oracle as orc
+    from paper_2509_14098_b200 import compare
+
+    rng = np.random.default_rng(5)
+    a = rng.normal(size=4096) + 1j * rng.normal(size=4096)
+    for pos in (0, 1234, 4095):
+        b = a.copy()
+        b[pos] = complex(float("nan"), 0.0)
+        assert math.isnan(orc.compare(a, b))
+        assert math.isnan(compare(a, b)), pos
+        assert math.isnan(compare(b, a)), pos
+    assert compare(a, a) == 0.0

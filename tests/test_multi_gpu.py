@@ -53,7 +53,8 @@ def test_dist_parity_colocated(world):
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "tools" / "dist_check.py"),
            "--quick", "--scale", "--colocate"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
-    tail = (r.stdout + r.stderr)[-3000:]
+    errs = [ln for ln in r.stderr.splitlines() if "Error" in ln or "error:" in ln or "Exception" in ln]
+    tail = r.stdout[-2000:] + "\n".join(errs[:40])
     assert r.returncode == 0, tail
     assert "0 mismatches" in r.stdout, tail
     print(r.stdout[-2000:])
