@@ -129,7 +129,8 @@ typedef struct svb_sweep_desc {
   int32_t nctab;                        /* per-tile scalar slots              */
   int32_t norm_slot;                    /* -1: no norm accumulation           */
   int32_t rb;                           /* register bits per thread (2^(K-rb) threads) */
-  int32_t pad0;
+  int32_t groups;                       /* generated kernels: tile groups per CTA
+                                           (0/1: one; 2: 2^(K-rb+1) threads) */
   int64_t ops_off, coef_off, tab_off;   /* byte offsets into prog             */
   int64_t cterm_off, cofs_off;          /* per-tile terms + CSR offsets       */
 } svb_sweep_desc;

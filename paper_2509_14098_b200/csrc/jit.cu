@@ -149,8 +149,9 @@ extern "C" int svb_jit_launch_sweep_part(void* kernel, svb_c128* state, const vo
     set_error("jit sweep: %zu bytes of shared memory exceed the 220 KB budget", smem);
     return SVB_ERANGE;
   }
+  const unsigned groups = d.groups > 1 ? (unsigned)d.groups : 1u;
   cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void*>(kernel), dim3((unsigned)grid),
-                                   dim3(1u << (d.K - d.rb)), args, smem, as_stream(stream));
+                                   dim3(groups << (d.K - d.rb)), args, smem, as_stream(stream));
   if (e != cudaSuccess) return cuda_status(e, "jit sweep launch");
   return SVB_OK;
 }

@@ -49,3 +49,30 @@ SVB_F void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memo
 SVB_F void st_stream(double2* p, double2 v) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
+
+// ---- two tile groups per CTA (jit.kernel_source_2g) ------------------------
+// mbarriers track the cp.async loads of each tile buffer: every thread of the
+// loading group arrives (noinc) once its prior cp.asyncs have landed, so the
+// barrier's count is the group size and the consuming group waits on the
+// phase parity of the buffer's use.
+SVB_F u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+SVB_F void mbar_init(unsigned long long* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+SVB_F void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+SVB_F void cp_async_mbar_arrive(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+SVB_F void mbar_wait_parity(unsigned long long* bar, u32 parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// named barrier of one tile group (id 0 is __syncthreads)
+SVB_F void bar_group(u32 id, u32 nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }

@@ -240,6 +240,8 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
         names, cubins = jitmod.build_kernels(dp.buf, sparse=sparse)
         out.zero_init = dict(jitmod._LAST_ZERO_INIT)
         out.sparse = sparse
+        for i, gcount in jitmod._LAST_GROUPS.items():  # launch geometry of two-group kernels
+            descs[i]["groups"] = gcount
         dev_index = device.index if device.index is not None else torch.cuda.current_device()
         out.kernels = [jitmod.load_kernel(n, c, dev_index) for n, c in zip(names, cubins)]
         out.jit_seconds = time.perf_counter() - t1

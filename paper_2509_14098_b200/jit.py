@@ -37,6 +37,8 @@ CTAB_AHEAD = os.environ.get("SVB200_JIT_CTAB_AHEAD", "1") not in ("0", "false", 
 NO_AHEAD_ZERO = os.environ.get("SVB200_JIT_NO_AHEAD_ZERO", "1") not in ("0", "false", "no")
 # stage changes that keep the warp-level thread bits move data with warp shuffles
 SHUFFLE_STAGES = os.environ.get("SVB200_JIT_SHUFFLE", "0") not in ("0", "false", "no")  # measured: slower
+# FP64-heavy sweeps run two tile groups per CTA (kernel_source_2g)
+GROUPS = os.environ.get("SVB200_JIT_GROUPS", "1") not in ("0", "false", "no")
 NVRTC_OPTS = ["--gpu-architecture=sm_100a", "--std=c++17", f"-I{CSRC}", "-lineinfo",
               "--extra-device-vectorization"]
 
@@ -528,6 +530,274 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     return "\n".join(L) + "\n"
 
 
+# sweeps whose FP64 work per amplitude reaches this many DFMA (a fused 4x4 is
+# 16) run two tile groups per CTA (kernel_source_2g)
+GROUPS_MIN_DFMA = float(os.environ.get("SVB200_JIT_GROUPS_MIN_DFMA", "48"))
+
+
+def dfma_per_amp(ops, rb: int) -> float:
+    """Rough FP64 FMA count per amplitude of a sweep's op list: a 4x4 on
+    register pairs 16, a 2x2 8, an H 1, phases ~4 (bookkeeping for the
+    tile-group choice, not the roofline)."""
+    n = 0.0
+    for op in ops:
+        k = int(op["kind"])
+        if k == prog.OP_U2:
+            n += 16
+        elif k == prog.OP_U1:
+            n += 8
+        elif k == prog.OP_H:
+            n += 1 + (4 if int(op["flags"]) & prog.F_PHASE else 0)
+        elif k in (prog.OP_PH, prog.OP_PHALL):
+            n += 4
+    return n
+
+
+def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: int = 0,
+                     sparse: tuple | None = None) -> str:
+    """Straight-line kernel for one FP64-heavy sweep with two tile groups.
+
+    A one-group CTA cannot overlap a register<->shared-memory stage with
+    FP64 work: all its warps meet at the stage barrier (round-1 ncu: FP64
+    pipe 67%, the heaviest QV sweep's time = FP64 time + stage time).  Here
+    the CTA has two groups of 2^(K-rb) threads working on alternate tiles
+    of the CTA's sequence (tile k -> group k % 2, buffer k % 3), each with
+    its own named barrier, so one group's stages and stores run while the
+    other computes.  Loads are cp.async into the buffer of tile k+3, issued
+    by the group that just stored tile k from that buffer and tracked by a
+    per-buffer mbarrier (cp.async.mbarrier.arrive) that the consuming group
+    waits on with the phase parity of the buffer's use.  Registers: 512
+    threads leave 128 per thread."""
+    K, D = desc["K"], desc["D"]
+    rb = int(desc["rb"])
+    NR = 1 << rb
+    NT = 1 << (K - rb)
+    tb = K - rb
+    tin = list(desc["tin"])[:K]
+    sw = list(desc["sw"])[:K]
+    st_dev = list(desc["st_dev"])[:K]
+    st_sw = list(desc["st_sw"])[:K]
+    st_flip = int(desc["st_flip"])
+    nct = int(desc["nctab"])
+    assert not desc.get("cbits"), "part launches keep the one-group kernel"
+    fbits = [b for b in range(D) if b not in tin]
+    fpos = {b: i for i, b in enumerate(fbits)}
+    fprime = list(fbits)
+    tinmask = sum(1 << b for b in tin)
+    ld_zero = 0
+    NTV = "ntiles"
+    dead_slabs = []
+    if sparse is not None:
+        supp, full_out = sparse
+        if supp is None:
+            fprime = []
+            NTV = "0ll"
+            if full_out:
+                dead_slabs = [(None, list(range(D)))]
+        else:
+            fprime = [b for b in fbits if (supp >> b) & 1]
+            NTV = f"{1 << len(fprime)}ll"
+            ld_zero = tinmask & ~supp
+            if full_out:
+                zs = sorted((b for b in fbits if not (supp >> b) & 1), reverse=True)
+                for j, z in enumerate(zs):
+                    dead_slabs.append((z, [b for b in range(D) if b not in zs[:j + 1]]))
+
+    def origin(var):
+        return _deposit(var, fprime) if fprime else "0ull"
+
+    def full_tid(var):
+        if sparse is not None:
+            return f"((long long)({_deposit(var, [fpos[b] for b in fprime])}))" if fprime else "0ll"
+        return var
+
+    L = []
+    w = L.append
+    w('#include "sweep_jit.cuh"')
+    w("// two tile groups")
+    w(f'extern "C" __global__ void __launch_bounds__({2 * NT}, 1)')
+    w(f"{name}(double2* __restrict__ state, const double2* __restrict__ tab, "
+      "const svb_cterm* __restrict__ cterms, const int* __restrict__ cofs, double* __restrict__ norm_out, "
+      "const u64 part_val, const u64 part_tid, const long long ntiles) {")
+    w("  extern __shared__ __align__(16) double2 smem[];")
+    w("  __shared__ double red[32];")
+    w("  __shared__ __align__(8) unsigned long long mbar[3];")
+    w(f"  const int grp = threadIdx.x >> {tb};")
+    w(f"  const int t = threadIdx.x & {NT - 1};")
+    w("  const u32 bar_id = 1u + (u32)grp;")
+    w(f"  double2* const ctab = smem + {3 << K} + grp * {max(nct, 1)};")
+    w(f"  const u64 ld_t = {_deposit('t', tin[:tb])};")
+    w(f"  const u32 lds_t = {_xor_img('t', sw[:tb])};")
+    w(f"  const u64 st_t = {_deposit('t', st_dev[:tb])};")
+    w(f"  const u32 sts_t = {_xor_img('t', st_sw[:tb])};")
+    if ld_zero:
+        w(f"  const bool ld_live = (ld_t & {ld_zero}ull) == 0ull;")
+    for off in sorted({int(op["tab"]) for op in ops if op["kind"] != prog.OP_STAGE and int(op["tab"]) >= 0}):
+        w(f"  const double2 tab{off} = __ldg(tab + {off} + t);")
+    stages = [op for op in ops if op["kind"] == prog.OP_STAGE]
+    stage_info = []
+    for si, st in enumerate(stages):
+        rm = int(st["rmask"])
+        regs = [k for k in range(K) if (rm >> k) & 1]
+        flags = int(st["flags"]) if not isinstance(st, dict) else int(st.get("flags", 0))
+        if flags & prog.F_TORDER:
+            comp = prog.unpack_order(int(st["pval"]), K - len(regs))
+        else:
+            comp = [k for k in range(K) if not (rm >> k) & 1]
+        w(f"  const u32 sb{si} = {_xor_img('t', [sw[k] for k in comp])};")
+        w(f"  const u64 db{si} = {_deposit('t', [tin[k] for k in comp])};")
+        offs = []
+        for v in range(NR):
+            o = 0
+            for q in range(rb):
+                if (v >> q) & 1:
+                    o ^= sw[regs[q]]
+            offs.append(o)
+        stage_info.append((regs, comp, offs))
+    TILE = 1 << K
+
+    def prefetch_items(buf, base):
+        for it in range(NR):
+            dev = 0
+            s_ = 0
+            for q in range(rb):
+                if (it >> q) & 1:
+                    dev |= 1 << tin[tb + q]
+                    s_ ^= sw[tb + q]
+            if dev & ld_zero:
+                w(f"      cp_async16_zero({buf} + (lds_t ^ {s_}u), state);")
+            elif ld_zero:
+                w(f"      cp_async16_pred({buf} + (lds_t ^ {s_}u), state + ({base} | ld_t | {dev}ull), "
+                  "ld_live, state);")
+            else:
+                w(f"      cp_async16({buf} + (lds_t ^ {s_}u), state + ({base} | ld_t | {dev}ull));")
+
+    w("  if (threadIdx.x == 0) {")
+    w("    for (int b = 0; b < 3; ++b) mbar_init(&mbar[b], " + str(NT) + "u);")
+    w("    mbar_init_fence();")
+    w("  }")
+    w("  __syncthreads();")
+    w("  double nrm = 0.0;")
+    if not zero_init:
+        # tiles 0 and 2 by group 0, tile 1 by group 1 (buffer = tile % 3)
+        w("  for (int k = grp; k < 3; k += 2) {")
+        w("    const long long pt = blockIdx.x + (long long)k * gridDim.x;")
+        w(f"    if (pt < {NTV}) {{")
+        w(f"      const u64 bq = {origin('pt')};")
+        prefetch_items(f"(smem + k * {TILE})", "bq")
+        w("    }")
+        w("    cp_async_mbar_arrive(&mbar[k]);")
+        w("  }")
+    w("  for (int k = grp;; k += 2) {")
+    w("    const long long tile_id = blockIdx.x + (long long)k * gridDim.x;")
+    w(f"    if (tile_id >= {NTV}) break;")
+    w("    const int b = k % 3;")
+    w(f"    double2* const tile = smem + b * {TILE};")
+    w(f"    const u64 base = {origin('tile_id')};")
+    if nct:
+        lut_off, nch = int(desc["lut_off"]), int(desc["lut_nch"])
+        residual = desc["residual"]
+        w(f"    {{ const long long ftid_ = {full_tid('tile_id')};")
+        w(f"    for (int i = t; i < {nct}; i += {NT}) {{")
+        w(f"      const double2* lt = tab + {lut_off} + i * {nch * 256};")
+        w("      double2 acc = __ldg(lt + (ftid_ & 255));")
+        for c in range(1, nch):
+            w(f"      acc = cmul(acc, __ldg(lt + {c * 256} + ((ftid_ >> {8 * c}) & 255)));")
+        if any(residual):
+            for s_, terms in enumerate(residual):
+                if not terms:
+                    continue
+                w(f"      if (i == {s_}) {{")
+                for mask, cval in terms:
+                    w(f"        if ((base & {int(mask)}ull) == {int(mask)}ull) "
+                      f"acc = cmulc(acc, {_lit(cval.real)}, {_lit(cval.imag)});")
+                w("      }")
+        w("      ctab[i] = acc;")
+        w("    } }")
+    if not zero_init:
+        w("    mbar_wait_parity(&mbar[b], (u32)((k / 3) & 1));")
+    w(f"    bar_group(bar_id, {NT}u);")
+    w(f"    double2 x[{NR}];")
+    cur = None
+    pending = []
+    for op in ops:
+        kind = int(op["kind"])
+        if kind == prog.OP_STAGE:
+            nxt = 0 if cur is None else cur + 1
+            for o in pending:
+                _emit_op(w, o, coef, cur, K, rb)
+            pending = []
+            if cur is not None:
+                _, _, offs = stage_info[cur]
+                for v in range(NR):
+                    w(f"    tile[sb{cur} ^ {offs[v]}u] = x[{v}];")
+                w(f"    bar_group(bar_id, {NT}u);")
+            _, _, offs = stage_info[nxt]
+            if nxt == 0 and zero_init:
+                for v in range(NR):
+                    w(f"    x[{v}] = make_double2(0.0, 0.0);")
+                if zero_init == 1:
+                    w("    if (base == 0ull && t == 0) x[0] = make_double2(1.0, 0.0);")
+            else:
+                for v in range(NR):
+                    w(f"    x[{v}] = tile[sb{nxt} ^ {offs[v]}u];")
+            cur = nxt
+            continue
+        pending.append(op)
+    for o in pending:
+        _emit_op(w, o, coef, cur, K, rb)
+    if cur is not None:
+        _, _, offs = stage_info[cur]
+        for v in range(NR):
+            w(f"    tile[sb{cur} ^ {offs[v]}u] = x[{v}];")
+    w(f"    bar_group(bar_id, {NT}u);")
+    for it in range(NR):  # store this tile, then the buffer takes tile k+3
+        dev = 0
+        s_ = 0
+        for q in range(rb):
+            if (it >> q) & 1:
+                dev |= 1 << st_dev[tb + q]
+                s_ ^= st_sw[tb + q]
+        w("    {")
+        w(f"      const double2 v = tile[sts_t ^ {s_}u];")
+        w("      nrm = fma(v.x, v.x, fma(v.y, v.y, nrm));")
+        w(f"      st_stream(state + (base | ((st_t | {dev}ull) ^ {st_flip}ull)), v);")
+        w("    }")
+    if not zero_init:
+        w(f"    bar_group(bar_id, {NT}u);")
+        w("    {")
+        w("      const long long nk = tile_id + 3ll * gridDim.x;")
+        w(f"      if (nk < {NTV}) {{")
+        w(f"        const u64 bn = {origin('nk')};")
+        prefetch_items("tile", "bn")
+        w("      }")
+        w("      cp_async_mbar_arrive(&mbar[b]);")
+        w("    }")
+    w("  }")
+    w("  cp_async_wait_all();")
+    for z, free in dead_slabs:
+        n = 1 << len(free)
+        one = f" | {1 << z}ull" if z is not None else ""
+        w("  {")
+        w(f"    const long long gs = (long long)gridDim.x * {2 * NT};")
+        w(f"    for (long long c = (long long)blockIdx.x * {2 * NT} + threadIdx.x; c < {n}ll; c += gs)")
+        w(f"      st_stream(state + (({_deposit('c', free)}){one}), make_double2(0.0, 0.0));")
+        w("  }")
+    w("  if (norm_out != nullptr) {")
+    for o in (16, 8, 4, 2, 1):
+        w(f"    nrm += __shfl_xor_sync(0xffffffffu, nrm, {o});")
+    w("    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;")
+    w("    __syncthreads();")
+    w("    if (threadIdx.x == 0) {")
+    w("      double s = 0.0;")
+    w(f"      for (int i = 0; i < {2 * NT // 32}; ++i) s += red[i];")
+    w("      atomicAdd(norm_out, s);")
+    w("    }")
+    w("  }")
+    w("}")
+    return "\n".join(L) + "\n"
+
+
 def _phase_base(w, op, coef_c0: complex, K: int, rb: int) -> None:
     """Emit `p` = const * per-tile slot * per-thread table * per-thread-bit slots.
 
@@ -660,6 +930,7 @@ def _emit_dfs(w, a: int, nt: int, c: list, fused_h: bool, rb: int, half=None) ->
 
 _mem_cache: dict = {}  # source hash -> cubin bytes
 _LAST_ZERO_INIT: dict = {}  # descriptors the last build_kernels synthesised from |0>
+_LAST_GROUPS: dict = {}  # descriptors the last build_kernels rendered with two tile groups
 _kernels: dict = {}  # (source hash, device) -> kernel handle
 
 
@@ -727,6 +998,7 @@ def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: in
         if supp is None or supp == 0:
             zero_init[i] = 2 if supp is None else 1
     used = {}
+    groups = {}
     for i, d in enumerate(buf.descs):
         ops = buf.ops[d["op_begin"]: d["op_begin"] + d["op_count"]]
         zi = zero_init.get(i, 0)
@@ -734,13 +1006,20 @@ def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: in
             raise ValueError(f"sweep {i} cannot synthesise |0...0> (no register stage)")
         if zi:
             used[i] = zi
-        body = kernel_source("KNAME", d, ops, buf.coef, zi, sparse.get(i))
+        two = (GROUPS and not d.get("cbits") and (1 << (int(d["K"]) - int(d["rb"]))) == 256
+               and dfma_per_amp(ops, int(d["rb"])) >= GROUPS_MIN_DFMA)
+        gen = kernel_source_2g if two else kernel_source
+        if two:
+            groups[i] = 2
+        body = gen("KNAME", d, ops, buf.coef, zi, sparse.get(i))
         h = hashlib.sha1(body.encode()).hexdigest()[:16]
         name = f"{prefix}_{h}"
         srcs.append(body.replace("KNAME", name))
         names.append(name)
     _LAST_ZERO_INIT.clear()
     _LAST_ZERO_INIT.update(used)
+    _LAST_GROUPS.clear()
+    _LAST_GROUPS.update(groups)
     # the processes of one node compile at the same time: share the host cores
     local = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
     threads = threads or max(1, min(32, (os.cpu_count() or 4) // max(local, 1)))

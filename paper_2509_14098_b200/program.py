@@ -69,7 +69,7 @@ DESC_DTYPE = np.dtype(
         ("st_flip", "<u8"),
         ("op_begin", "<i4"), ("op_count", "<i4"),
         ("nctab", "<i4"), ("norm_slot", "<i4"),
-        ("rb", "<i4"), ("pad0", "<i4"),
+        ("rb", "<i4"), ("groups", "<i4"),
         ("ops_off", "<i8"), ("coef_off", "<i8"), ("tab_off", "<i8"),
         ("cterm_off", "<i8"), ("cofs_off", "<i8"),
     ],

@@ -78,6 +78,11 @@ def scale_checks(me, world):
         names.append((f"qft34_h{34 - lg}-12", 0))
     for name, x in names:
         plan = planmod.load(str(ROOT / "plans" / f"{name}.json.gz"))
+        if "--colocate" in sys.argv:  # all processes share one GPU's memory
+            from paper_2509_14098_b200 import comm
+
+            comm.release_arenas()
+            torch.cuda.empty_cache()
         rows = (1 << plan.g) // world
         init = basis_blocks(plan, x, me * rows, rows, "cuda") if x else None
         res = run_plan(plan, initial=init)
@@ -97,7 +102,8 @@ def scale_checks(me, world):
         plan = planmod.load(str(ROOT / "plans" / f"{name}.json.gz"))
         if (1 << plan.g) < world:
             continue
-        if plan.d - plan.g >= 32:  # 64+ GiB per GPU: return the pooled buffers of earlier runs first
+        if plan.d - plan.g >= 32 or "--colocate" in sys.argv:
+            # 64+ GiB per GPU, or every process on one GPU: return the pooled buffers of earlier runs first
             from paper_2509_14098_b200 import comm
 
             comm.release_arenas()
