@@ -151,6 +151,8 @@ def _dist_info(group=None):
 # runs from |0...0> compute only the support of the state until it covers
 # the device (program.sparse_start)
 SPARSE_START = os.environ.get("SVB200_SPARSE_START", "1") not in ("0", "false", "no")
+# generated kernels compile in the background; each launch waits only for its own
+PIPELINED_JIT = os.environ.get("SVB200_JIT_PIPELINE", "1") not in ("0", "false", "no")
 # per-launch CUDA events around every sweep (bench.py's roofline); off by default
 PROFILE_SWEEPS = False
 _prof_log: list | None = None  # (descriptor, bytes, start event, end event) of the current run
@@ -185,6 +187,8 @@ class _Compiled:
     kernels: list | None = None  # per-descriptor JIT kernel handles (None: interpreter)
     desc_bytes: list = field(default_factory=list)  # per descriptor: HBM bytes one full launch moves
     norm_alias: dict = field(default_factory=dict)  # slot -> slot whose sweep measured its norm
+    dev_index: int = 0
+    wait_seconds: float = 0.0  # host time blocked on kernels still compiling (pipelined JIT)
     jit_seconds: float = 0.0
     zero_init: dict = field(default_factory=dict)  # descriptors that synthesise |0...0>
     sparse: dict = field(default_factory=dict)  # descriptor -> (support, full_out), prog.sparse_start
@@ -237,13 +241,17 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
 
         t1 = time.perf_counter()
         sparse = prog.sparse_start(dp, geo.D, geo.rank_base == 0) if (zero_start and SPARSE_START) else {}
-        names, cubins = jitmod.build_kernels(dp.buf, sparse=sparse)
+        names, slots = jitmod.build_kernels(dp.buf, sparse=sparse, lazy=PIPELINED_JIT)
         out.zero_init = dict(jitmod._LAST_ZERO_INIT)
         out.sparse = sparse
         for i, gcount in jitmod._LAST_GROUPS.items():  # launch geometry of two-group kernels
             descs[i]["groups"] = gcount
         dev_index = device.index if device.index is not None else torch.cuda.current_device()
-        out.kernels = [jitmod.load_kernel(n, c, dev_index) for n, c in zip(names, cubins)]
+        out.dev_index = dev_index
+        if PIPELINED_JIT:  # resolved at first launch (_kernel): early sweeps run while later ones compile
+            out.kernels = list(slots)
+        else:
+            out.kernels = [jitmod.load_kernel(n, c, dev_index) for n, c in zip(names, slots)]
         out.jit_seconds = time.perf_counter() - t1
     out.desc_bytes = [sum(prog.sparse_bytes(d, out.sparse.get(i))) for i, d in enumerate(dp.buf.descs)]
     _compile_cache.clear()  # keep one plan resident
@@ -572,6 +580,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
                 fail(PlanInvalid("Alloc payload disagrees with plan shape"))
             compiled = compile_plan(plan, geo_eff, device, jit, zero_start=initial is None)
             stats.compile_seconds = compiled.compile_seconds + compiled.jit_seconds
+            wait0 = compiled.wait_seconds
             # when the first sweep synthesises |0...0> the state needs no memset
             from . import comm
 
@@ -667,6 +676,10 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
     if state is None:
         raise PlanInvalid("plan never allocated state")
     mat = compiled.steps.get(None)
+    if mat is not None and compiled.kernels is not None:  # materialisation kernels, before the clock stops
+        for di in range(mat.first, mat.first + mat.count):
+            _kernel(compiled, di)
+    stats.compile_seconds += compiled.wait_seconds - wait0  # launches that waited for their kernel
     if mat is not None:  # restore the reference layout
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -828,7 +841,7 @@ def _launch_part(compiled, di, state, norms, grid_limit, stream, cbits, c) -> No
     val, tid = _part_values(cbits, c, fbits)
     ntiles = 1 << (D - K - len(cbits))
     ev = _prof_begin()
-    rc = lib.svb_jit_launch_sweep_part(compiled.kernels[di], state.buf.data_ptr(), compiled.blob.data_ptr(),
+    rc = lib.svb_jit_launch_sweep_part(_kernel(compiled, di), state.buf.data_ptr(), compiled.blob.data_ptr(),
                                        compiled.descs[di:di + 1].ctypes.data,
                                        norms.data_ptr() if norms is not None else None,
                                        grid_limit, val, tid, ntiles, stream)
@@ -916,6 +929,22 @@ def _remap_overlapped(state, xst, geo, group, ovl):
     return launches, e0, e1
 
 
+def _kernel(compiled, di: int) -> int:
+    """Kernel handle of descriptor di, waiting for its compile if needed."""
+    k = compiled.kernels[di]
+    if isinstance(k, int):
+        return k
+    import time
+
+    from . import jit as jitmod
+
+    t0 = time.perf_counter()
+    h = jitmod.load_kernel(k.name, k.cubin(), compiled.dev_index)
+    compiled.wait_seconds += time.perf_counter() - t0
+    compiled.kernels[di] = h
+    return h
+
+
 def _prof_begin():
     if _prof_log is None:
         return None
@@ -957,7 +986,7 @@ def _run_descs(compiled, first, count, state, rows_eff, L, norms, grid_limit, st
             launches += 1 << len(cb)
             continue
         ev = _prof_begin()
-        rc = lib.svb_jit_launch_sweep(compiled.kernels[first + i], state.buf.data_ptr(),
+        rc = lib.svb_jit_launch_sweep(_kernel(compiled, first + i), state.buf.data_ptr(),
                                       compiled.blob.data_ptr(), descs[i:i + 1].ctypes.data, nptr,
                                       grid_limit, stream)
         _native.check(rc, "svb_jit_launch_sweep")

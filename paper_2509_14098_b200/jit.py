@@ -945,16 +945,72 @@ def _header_key() -> str:
     return _HEADER_KEY
 
 
-def _compile(src: str, name: str) -> bytes:
-    h = hashlib.sha256((src + "\0" + " ".join(NVRTC_OPTS) + "\0" + _header_key()).encode()).hexdigest()
+def _key(src: str) -> str:
+    return hashlib.sha256((src + "\0" + " ".join(NVRTC_OPTS) + "\0" + _header_key()).encode()).hexdigest()
+
+
+def _cached(h: str) -> bytes | None:
     hit = _mem_cache.get(h)
     if hit is not None:
         return hit
     path = CACHE_DIR / f"{h}.cubin"
-    if path.exists():
+    try:
         data = path.read_bytes()
-        _mem_cache[h] = data
-        return data
+    except OSError:
+        return None
+    _mem_cache[h] = data
+    return data
+
+
+LOCK_STALE_S = 120.0
+
+
+def _compile(src: str, name: str) -> bytes:
+    """NVRTC-compile one kernel, or take it from the memory / disk cache.
+
+    Processes of one node share the disk cache: a kernel another process
+    is compiling (its lock file exists) is waited for instead of compiled
+    twice, so ranks with identical sweeps split the compile work."""
+    h = _key(src)
+    hit = _cached(h)
+    if hit is not None:
+        return hit
+    lock = CACHE_DIR / f"{h}.lock"
+    try:
+        CACHE_DIR.mkdir(parents=True, exist_ok=True)
+        fd = os.open(lock, os.O_CREAT | os.O_EXCL | os.O_WRONLY)
+        os.close(fd)
+        owned = True
+    except FileExistsError:
+        owned = False
+    except OSError:
+        owned = True  # no writable cache: compile here
+    if not owned:
+        import time
+
+        while True:
+            hit = _cached(h)
+            if hit is not None:
+                return hit
+            try:
+                age = time.time() - lock.stat().st_mtime
+            except OSError:
+                age = None  # the owner finished (or failed): compile here
+            if age is None or age > LOCK_STALE_S:
+                break
+            time.sleep(0.005)
+    try:
+        return _nvrtc(src, name, h)
+    finally:
+        if owned:
+            try:
+                lock.unlink()
+            except OSError:
+                pass
+
+
+def _nvrtc(src: str, name: str, h: str) -> bytes:
+    path = CACHE_DIR / f"{h}.cubin"
     lib = _native.load()
     opts = (ctypes.c_char_p * len(NVRTC_OPTS))(*[o.encode() for o in NVRTC_OPTS])
     image = ctypes.c_void_p()
@@ -983,7 +1039,7 @@ def _compile(src: str, name: str) -> bytes:
 
 
 def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: int | None = None,
-                  zero_init: dict | None = None, sparse: dict | None = None):
+                  zero_init: dict | None = None, sparse: dict | None = None, lazy: bool = False):
     """Generate + compile one kernel per sweep descriptor; returns (names, cubins).
 
     zero_init maps descriptor index -> 1/2 for sweeps whose input is known to
@@ -1020,12 +1076,58 @@ def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: in
     _LAST_ZERO_INIT.update(used)
     _LAST_GROUPS.clear()
     _LAST_GROUPS.update(groups)
-    # the processes of one node compile at the same time: share the host cores
+    slots = compile_async(srcs, names, threads)
+    if lazy:
+        return names, slots
+    return names, [sl.cubin() for sl in slots]
+
+
+class KernelSlot:
+    """A kernel being compiled in the background: cubin() blocks until its
+    image exists (from this process's pool or from another process through
+    the disk cache), so sweeps can launch while later sweeps compile."""
+
+    def __init__(self, name: str, h: str, future):
+        self.name, self.h, self.future = name, h, future
+
+    def cubin(self) -> bytes:
+        import time
+
+        while True:
+            if self.future.done():
+                return self.future.result()
+            hit = _cached(self.h)
+            if hit is not None:
+                return hit
+            time.sleep(0.001)
+
+
+_POOL = None
+
+
+def compile_async(srcs: list, names: list, threads: int | None = None) -> list:
+    """Submit the kernels to the compile pool in launch order (identical
+    sources once); the processes of one node start at different offsets and
+    share results through the disk cache."""
+    global _POOL
     local = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
-    threads = threads or max(1, min(32, (os.cpu_count() or 4) // max(local, 1)))
-    with ThreadPoolExecutor(max_workers=threads) as ex:
-        cubins = list(ex.map(lambda sn: _compile(*sn), zip(srcs, names)))
-    return names, cubins
+    lrank = int(os.environ.get("LOCAL_RANK", "0"))
+    if _POOL is None:
+        # the processes of one node compile at the same time: share the host cores
+        n = threads or max(1, min(32, (os.cpu_count() or 4) // max(local, 1)))
+        _POOL = ThreadPoolExecutor(max_workers=n, thread_name_prefix="svb-nvrtc")
+    keys = [_key(src) for src in srcs]
+    first = {}
+    for i, h in enumerate(keys):
+        first.setdefault(h, i)
+    order = sorted(first.values())
+    if local > 1 and order:  # rotate: rank r begins its share of the list, then wraps
+        r = (lrank * len(order)) // local
+        order = order[:1] + order[r:] + order[1:r] if r > 1 else order
+    futs = {}
+    for i in order:
+        futs[keys[i]] = _POOL.submit(_compile, srcs[i], names[i])
+    return [KernelSlot(names[i], keys[i], futs[keys[i]]) for i in range(len(srcs))]
 
 
 def load_kernel(name: str, cubin: bytes, device_index: int):
