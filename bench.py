@@ -85,6 +85,72 @@ def plan_bytes(plan) -> int:
     return fused * 32 * (1 << plan.d)
 
 
+FP64_PEAK_TFS = 33.2  # DFMA, 16 warps/SM, measured on B200 (profiles/r01_fp64_dmma_vs_dfma.txt)
+
+
+def sass_fp64_flops_per_tile(cubin: bytes) -> int:
+    """FP64 flops one thread issues per tile of a generated sweep kernel:
+    the kernels are straight-line per tile, so the static SASS count of
+    DFMA (2 flops), DMUL and DADD (1 each) is the executed count (the
+    per-kernel prologue and the norm epilogue are a few instructions)."""
+    import re
+    import tempfile
+
+    with tempfile.NamedTemporaryFile(suffix=".cubin") as fh:
+        fh.write(cubin)
+        fh.flush()
+        sass = subprocess.run(["cuobjdump", "-sass", fh.name], capture_output=True, text=True).stdout
+    n_fma = len(re.findall(r"\bDFMA\b", sass))
+    n_other = len(re.findall(r"\bD(?:MUL|ADD)\b", sass))
+    return 2 * n_fma + n_other
+
+
+def fp64_all_sweeps(plan_, prof: dict, compute_s_per_step: float, steps: int):
+    """Executed FP64 flops of every sweep of one circuit / its sweep time."""
+    from paper_2509_14098_b200 import executor, jit as jitmod
+
+    comp = None
+    for _, (pl, c) in executor._compile_cache.items():
+        if pl is plan_:
+            comp = c
+    if comp is None or not comp.kernel_keys:
+        return None
+    total = 0
+    for di in range(len(comp.kernel_keys)):
+        cub = jitmod._cached(comp.kernel_keys[di])
+        if cub is None:
+            return None
+        d = comp.descs[di]
+        K, D, rb = int(d["K"]), int(d["D"]), int(d["rb"])
+        total += sass_fp64_flops_per_tile(cub) * (1 << (K - rb)) * (1 << (D - K))
+    achieved = total / compute_s_per_step / 1e12
+    return {"flops_per_step": total, "achieved": achieved, "frac": achieved / FP64_PEAK_TFS}
+
+
+def fp64_roofline(plan_, di: int, launch_ms: float):
+    """Executed FP64 TF/s of sweep di of the plan's compiled program."""
+    from paper_2509_14098_b200 import executor, jit as jitmod
+
+    comp = None
+    for _, (pl, c) in executor._compile_cache.items():
+        if pl is plan_:
+            comp = c
+    if comp is None or not comp.kernel_keys:
+        return None
+    cub = jitmod._cached(comp.kernel_keys[di])
+    if cub is None:
+        return None
+    d = comp.descs[di]
+    K, D, rb = int(d["K"]), int(d["D"]), int(d["rb"])
+    per_thread = sass_fp64_flops_per_tile(cub)
+    flops = per_thread * (1 << (K - rb)) * (1 << (D - K))
+    achieved = flops / (launch_ms / 1e3) / 1e12
+    return {"bound": "fp64", "achieved": achieved, "peak": FP64_PEAK_TFS, "unit": "TFLOP/s",
+            "frac": achieved / FP64_PEAK_TFS, "flops_per_launch": flops,
+            "flops_note": "static SASS count of DFMA (x2), DMUL, DADD per thread per tile x threads x tiles",
+            "peak_source": "measured DFMA throughput, 16 warps/SM (profiles/r01_fp64_dmma_vs_dfma.txt)"}
+
+
 def peak_hbm() -> tuple[float, str]:
     try:
         return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
@@ -389,8 +455,9 @@ def main() -> None:
             "sweeps_per_step": a3["sweeps"] // k3,
             "sweeps_hbm_frac": a3["sweep_bytes"] / a3["compute_s"] / 1e9 / peak,
             "dominant": {"sweep": di3, "launch_ms": ms3, "hbm_frac": b3 / (ms3 / 1e3) / 1e9 / peak,
-                         "share_of_sweep_time": sh3},
-            "compile_ms": 1e3 * a3["stats"].compile_seconds}
+                         "share_of_sweep_time": sh3, "fp64": fp64_roofline(qvp, di3, ms3)},
+            "compile_ms": 1e3 * a3["stats"].compile_seconds,
+            "fp64_all_sweeps": fp64_all_sweeps(qvp, a3["prof"], a3["compute_s"] / k3, k3)}
 
     traffic = fp64 = None
     prof = ROOT / "profiles" / "traffic.json"

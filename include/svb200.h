@@ -270,6 +270,36 @@ int svb_stream_wait_u32(void* addr, uint32_t value, void* stream);
  *   one purpose (uploads, downloads, overlapped remap chunks); never freed.
  *   Dedicated handles never alias each other or torch's pooled streams. */
 int svb_stream_create(void** stream);
+/* ------------------------------------------------------------------------
+ * 7. numpy-identical sampling (paper_2509_14098_b200/sampling.py), replacing
+ *    svpart/executor.py:375-383 (probs = |psi|^2 / sum; rng.choice(p=probs)).
+ *
+ * svb_probs_numpy: |a|^2 of a shard with numpy's complex absolute value,
+ *   written in basis-sorted shard order (perm: storage bit -> sorted bit).
+ * svb_deposit_scatter: dst[deposit(i, dst_bits) | or_val] = src[i].
+ * svb_pairwise_sum: numpy's pairwise sum of 2^D doubles into *out.
+ * svb_div_scalar: x[i] /= *denom (device scalar).
+ * svb_cdf_chunk_totals / svb_cdf_walk: the exact sequential cumsum of n
+ *   doubles at every chunk end (svb_cdf_chunk_elems() elements per chunk),
+ *   from the exact start *c_in; cstart holds approximate chunk starts.
+ * svb_cdf_search: per shot the first element whose fl(c / c_last) exceeds
+ *   u (numpy searchsorted side="right"), over the chunk ends of all
+ *   processes; out[s] = global index, or -1 if another process owns it.
+ * ---------------------------------------------------------------------- */
+int64_t svb_cdf_chunk_elems(void);
+int svb_probs_numpy(const svb_c128* shard, int D, const int32_t* perm, double* out, void* stream);
+int svb_deposit_scatter(const double* src, int64_t n, int nbits, const int32_t* dst_bits, uint64_t or_val,
+                        double* dst, void* stream);
+size_t svb_pairwise_scratch_bytes(int D);
+int svb_pairwise_sum(const double* x, int D, double* out, void* scratch, void* stream);
+int svb_div_scalar(double* x, int64_t n, const double* denom, void* stream);
+size_t svb_cdf_scratch_bytes(int64_t n);
+int svb_cdf_chunk_totals(const double* q, int64_t n, double* tot, void* stream);
+int svb_cdf_walk(const double* q, int64_t n, const double* cstart, const double* tot, void* fn_scratch,
+                 const double* c_in, double* cend, long long* nslow, void* stream);
+int svb_cdf_search(const double* q, int64_t n, const double* cend_all, int64_t nchunks_all, int64_t my_lo,
+                   int64_t my_hi, double c_last, const double* u, int64_t nshots, int64_t index_base,
+                   int64_t* out, void* stream);
 /* svb_copy: n-amplitude SM copy; either pointer may be a mapped peer's. */
 int svb_copy(svb_c128* dst, const svb_c128* src, int64_t n, int grid_limit, void* stream);
 int svb_peer_swap(svb_c128* local, void* const* peers, int npeers, int64_t rows, int L,

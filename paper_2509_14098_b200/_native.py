@@ -62,6 +62,16 @@ _SIGS = {
     "svb_stream_write_u32": ([_vp, _u32, _vp], _int),
     "svb_stream_wait_u32": ([_vp, _u32, _vp], _int),
     "svb_stream_create": ([_c.POINTER(_vp)], _int),
+    "svb_cdf_chunk_elems": ([], _i64),
+    "svb_probs_numpy": ([_vp, _int, _pi32, _vp, _vp], _int),
+    "svb_deposit_scatter": ([_vp, _i64, _int, _pi32, _c.c_uint64, _vp, _vp], _int),
+    "svb_pairwise_scratch_bytes": ([_int], _sz),
+    "svb_pairwise_sum": ([_vp, _int, _vp, _vp, _vp], _int),
+    "svb_div_scalar": ([_vp, _i64, _vp, _vp], _int),
+    "svb_cdf_scratch_bytes": ([_i64], _sz),
+    "svb_cdf_chunk_totals": ([_vp, _i64, _vp, _vp], _int),
+    "svb_cdf_walk": ([_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
+    "svb_cdf_search": ([_vp, _i64, _vp, _i64, _i64, _i64, _c.c_double, _vp, _i64, _i64, _vp, _vp], _int),
     "svb_copy": ([_vp, _vp, _i64, _int, _vp], _int),
     "svb_peer_swap": ([_vp, _vp, _int, _i64, _int, _pi32, _int, _vp, _vp, _vp, _vp, _int, _int, _vp], _int),
 }

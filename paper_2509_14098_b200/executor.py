@@ -188,6 +188,8 @@ class _Compiled:
     desc_bytes: list = field(default_factory=list)  # per descriptor: HBM bytes one full launch moves
     norm_alias: dict = field(default_factory=dict)  # slot -> slot whose sweep measured its norm
     dev_index: int = 0
+    kernel_names: list = field(default_factory=list)
+    kernel_keys: list = field(default_factory=list)  # JIT cache keys (jit._cached) of the cubins
     wait_seconds: float = 0.0  # host time blocked on kernels still compiling (pipelined JIT)
     jit_seconds: float = 0.0
     zero_init: dict = field(default_factory=dict)  # descriptors that synthesise |0...0>
@@ -248,8 +250,10 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
             descs[i]["groups"] = gcount
         dev_index = device.index if device.index is not None else torch.cuda.current_device()
         out.dev_index = dev_index
+        out.kernel_names = list(names)
         if PIPELINED_JIT:  # resolved at first launch (_kernel): early sweeps run while later ones compile
             out.kernels = list(slots)
+            out.kernel_keys = [sl.h for sl in slots]
         else:
             out.kernels = [jitmod.load_kernel(n, c, dev_index) for n, c in zip(names, slots)]
         out.jit_seconds = time.perf_counter() - t1

@@ -688,6 +688,14 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
         w("    }")
         w("    cp_async_mbar_arrive(&mbar[k]);")
         w("  }")
+    # start the groups half a tile apart: group 1 waits until group 0 is in
+    # the middle of its first tile, so one group's stages and stores fall in
+    # the other's FP64 phase (started together they stay in lockstep)
+    nst = len(stage_info)
+    mid = nst // 2 if nst >= 2 else None
+    if mid is not None:
+        w("  bool offset_pending = grp == 0;")
+        w(f"  if (grp == 1) bar_group(3u, {2 * NT}u);")
     w("  for (int k = grp;; k += 2) {")
     w("    const long long tile_id = blockIdx.x + (long long)k * gridDim.x;")
     w(f"    if (tile_id >= {NTV}) break;")
@@ -741,6 +749,8 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
             else:
                 for v in range(NR):
                     w(f"    x[{v}] = tile[sb{nxt} ^ {offs[v]}u];")
+            if nxt == mid:
+                w(f"    if (offset_pending) {{ bar_group(3u, {2 * NT}u); offset_pending = false; }}")
             cur = nxt
             continue
         pending.append(op)
@@ -774,6 +784,8 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
         w("      cp_async_mbar_arrive(&mbar[b]);")
         w("    }")
     w("  }")
+    if mid is not None:  # group 0 had no tile: release group 1
+        w(f"  if (offset_pending) bar_group(3u, {2 * NT}u);")
     w("  cp_async_wait_all();")
     for z, free in dead_slabs:
         n = 1 << len(free)
