@@ -300,6 +300,11 @@ int svb_cdf_walk(const double* q, int64_t n, const double* cstart, const double*
 int svb_cdf_search(const double* q, int64_t n, const double* cend_all, int64_t nchunks_all, int64_t my_lo,
                    int64_t my_hi, double c_last, const double* u, int64_t nshots, int64_t index_base,
                    int64_t* out, void* stream);
+/* svb_gather_bits: dst[t] = src[P(base + t)], t < count, with
+ *   P(f) = sum_k bit_k(f) << perm[k] (one chunk of a permuted order: the
+ *   chunked gather of a sharded state, svpart/executor.py:310-326). */
+int svb_gather_bits(const svb_c128* src, int nbits, const int32_t* perm, uint64_t base, int64_t count,
+                    svb_c128* dst, void* stream);
 /* svb_copy: n-amplitude SM copy; either pointer may be a mapped peer's. */
 int svb_copy(svb_c128* dst, const svb_c128* src, int64_t n, int grid_limit, void* stream);
 int svb_peer_swap(svb_c128* local, void* const* peers, int npeers, int64_t rows, int L,

@@ -67,7 +67,26 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stderr}")
     os.replace(tmp, LIB)
+    build_native_host(force=True)
     return LIB
+
+
+NATIVE_HOST_SRC = ROOT / "native_host" / "svb_run.cpp"
+NATIVE_HOST = ROOT / "native_host" / "svb_run"
+
+
+def build_native_host(force: bool = False) -> Path:
+    """native_host/svb_run: the C++ host that runs a program file
+    (program_file.py) through include/svb200.h, without Python."""
+    if not force and NATIVE_HOST.exists() and NATIVE_HOST.stat().st_mtime > max(
+            NATIVE_HOST_SRC.stat().st_mtime, LIB.stat().st_mtime):
+        return NATIVE_HOST
+    cmd = [_nvcc(), "-std=c++17", "-O2", "-I", str(INCLUDE), str(NATIVE_HOST_SRC), "-o", str(NATIVE_HOST),
+           "-L", str(PKG), "-lsvb200", "-lcudart", "-Xlinker", f"-rpath,$ORIGIN/../{PKG.name}"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"native host build failed:\n{r.stderr}")
+    return NATIVE_HOST
 
 
 if __name__ == "__main__":

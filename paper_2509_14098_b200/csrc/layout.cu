@@ -101,6 +101,205 @@ __global__ void k_bitperm(const double2* __restrict__ src, double2* __restrict__
   }
 }
 
+// ---- tiled bit permutation ---------------------------------------------
+// A tile is the set of elements that differ only in the tile bits T: T holds
+// the low source bits (coalesced 16-byte loads in runs of 2^a) and the
+// source bits that land on the low destination bits (coalesced stores),
+// padded with further low source bits up to kTileBits.  A CTA loads a tile
+// into shared memory in source order and writes it out in destination
+// order; the XOR swizzle keeps both access patterns conflict free.  With
+// src == dst the permutation must map every tile onto itself (bit swaps
+// whose bits are all tile bits): the swap is then in place.
+constexpr int kTileBits = 10;
+constexpr int kTileThreads = 256;
+
+struct TilePerm {
+  int nt;                        // tile bits
+  int nrest;                     // non-tile source bits (tile index), ascending
+  int rest[SVB_MAX_DEV_BITS];
+  uint64_t ld_lo[32], ld_hi[32];  // load-order index -> source offset bits
+  uint64_t st_lo[32], st_hi[32];  // store-order index -> destination offset bits
+  uint16_t jmap_lo[32], jmap_hi[32];  // store-order index -> swizzled smem slot
+  uint32_t swz_lo[32], swz_hi[32];    // load-order index -> swizzled smem slot
+  int nchunks;
+  uint64_t plut[5 * 256];        // P on source indices (tile bases)
+};
+
+__global__ void __launch_bounds__(kTileThreads) k_tperm(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                        const __grid_constant__ TilePerm tp, uint64_t ntiles) {
+  extern __shared__ __align__(16) double2 tile[];
+  __shared__ uint64_t plut[5 * 256];
+  // per-lane table lookups from shared memory (parameter-space reads with
+  // lane-varying indices would serialise in the constant cache)
+  __shared__ uint64_t ld_lo[32], ld_hi[32], st_lo[32], st_hi[32];
+  __shared__ uint32_t sw_lo[32], sw_hi[32], jm_lo[32], jm_hi[32];
+  for (int i = threadIdx.x; i < tp.nchunks * 256; i += blockDim.x) plut[i] = tp.plut[i];
+  if (threadIdx.x < 32) {
+    const int v = threadIdx.x;
+    ld_lo[v] = tp.ld_lo[v];
+    ld_hi[v] = tp.ld_hi[v];
+    st_lo[v] = tp.st_lo[v];
+    st_hi[v] = tp.st_hi[v];
+    sw_lo[v] = tp.swz_lo[v];
+    sw_hi[v] = tp.swz_hi[v];
+    jm_lo[v] = tp.jmap_lo[v];
+    jm_hi[v] = tp.jmap_hi[v];
+  }
+  __syncthreads();
+  const int n = 1 << tp.nt;
+  for (uint64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    uint64_t sb = 0;
+    for (int i = 0; i < tp.nrest; ++i) sb |= ((ti >> i) & 1ull) << tp.rest[i];
+    uint64_t db = 0;
+    for (int c = 0; c < tp.nchunks; ++c) db |= plut[c * 256 + ((sb >> (8 * c)) & 255)];
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+      tile[sw_lo[j & 31] ^ sw_hi[j >> 5]] = src[sb | ld_lo[j & 31] | ld_hi[j >> 5]];
+    __syncthreads();
+    for (int k = threadIdx.x; k < n; k += blockDim.x)
+      st_stream(dst + (db | st_lo[k & 31] | st_hi[k >> 5]), tile[jm_lo[k & 31] ^ jm_hi[k >> 5]]);
+    __syncthreads();
+  }
+}
+
+// build the tile geometry of permutation perm (source bit k -> perm[k]);
+// inplace: the tile must be closed under perm.  Returns false when no tile
+// of at most kTileBits bits exists (the caller uses the element kernel).
+bool make_tile_perm(int nbits, const int32_t* perm, bool inplace, TilePerm& tp) {
+  if (nbits < 1 || nbits > SVB_MAX_DEV_BITS) return false;
+  int inv[64];
+  for (int k = 0; k < nbits; ++k) inv[perm[k]] = k;
+  const int a = nbits < 5 ? nbits : 5;
+  bool in_t[64] = {false};
+  int cnt = 0;
+  auto add = [&](int b) {
+    if (!in_t[b]) {
+      in_t[b] = true;
+      ++cnt;
+    }
+  };
+  for (int b = 0; b < a; ++b) add(b);
+  for (int b = 0; b < a; ++b) add(inv[b]);
+  if (inplace) {  // every moving bit in the tile, closed under perm: the tile maps onto itself
+    for (int b = 0; b < nbits; ++b)
+      if (perm[b] != b) add(b);
+    bool grew = true;
+    while (grew) {
+      grew = false;
+      for (int b = 0; b < nbits; ++b)
+        if (in_t[b] && !in_t[perm[b]]) {
+          add(perm[b]);
+          grew = true;
+        }
+    }
+    for (int b = 0; b < nbits; ++b)
+      if (!in_t[b] && perm[b] != b) return false;  // a moving bit outside the tile
+  }
+  if (cnt > kTileBits) return false;
+  for (int b = 0; b < nbits && cnt < kTileBits; ++b)
+    if (!in_t[b] && (!inplace || perm[b] == b)) add(b);
+  const int nt = cnt;
+  int src_t[kTileBits], dst_t[kTileBits], ns = 0;
+  for (int b = 0; b < nbits; ++b)
+    if (in_t[b]) src_t[ns++] = b;
+  int nd = 0;
+  for (int b = 0; b < nbits; ++b)
+    if (in_t[inv[b]]) dst_t[nd++] = b;
+  tp.nt = nt;
+  tp.nrest = 0;
+  for (int b = 0; b < nbits; ++b)
+    if (!in_t[b]) tp.rest[tp.nrest++] = b;
+  // load-order position of each store-order bit
+  int pos_of_src[64];
+  for (int i = 0; i < nt; ++i) pos_of_src[src_t[i]] = i;
+  int jpos[kTileBits];
+  for (int i = 0; i < nt; ++i) jpos[i] = pos_of_src[inv[dst_t[i]]];
+  // swizzle: load positions >= 3 that hold the low 3 store bits are folded
+  // onto the low slot bits the low 3 store bits do not already occupy
+  int fold_from[3], fold_to[3], nf = 0;
+  bool low_used[3] = {false, false, false};
+  for (int i = 0; i < 3 && i < nt; ++i)
+    if (jpos[i] < 3) low_used[jpos[i]] = true;
+  int free_low[3], nfl = 0;
+  for (int b = 0; b < 3 && b < nt; ++b)
+    if (!low_used[b]) free_low[nfl++] = b;
+  for (int i = 0; i < 3 && i < nt; ++i)
+    if (jpos[i] >= 3) {
+      fold_from[nf] = jpos[i];
+      fold_to[nf] = free_low[nf];
+      ++nf;
+    }
+  auto swz = [&](uint32_t j) {
+    uint32_t x = j;
+    for (int f = 0; f < nf; ++f) x ^= ((j >> fold_from[f]) & 1u) << fold_to[f];
+    return x;
+  };
+  for (int v = 0; v < 32; ++v) {
+    uint64_t llo = 0, lhi = 0, slo = 0, shi = 0;
+    uint32_t jlo = 0, jhi = 0;
+    for (int i = 0; i < 5; ++i) {
+      if ((v >> i) & 1) {
+        if (i < nt) {
+          llo |= uint64_t(1) << src_t[i];
+          slo |= uint64_t(1) << dst_t[i];
+          jlo |= 1u << jpos[i];
+        }
+        if (i + 5 < nt) {
+          lhi |= uint64_t(1) << src_t[i + 5];
+          shi |= uint64_t(1) << dst_t[i + 5];
+          jhi |= 1u << jpos[i + 5];
+        }
+      }
+    }
+    tp.ld_lo[v] = llo;
+    tp.ld_hi[v] = lhi;
+    tp.st_lo[v] = slo;
+    tp.st_hi[v] = shi;
+    // swizzle is linear (XOR of bit images): split over the two halves
+    tp.swz_lo[v] = swz((uint32_t)v);  // linear over XOR: slot(j) = slot(j & 31) ^ slot(j & ~31)
+    tp.swz_hi[v] = swz((uint32_t)v << 5);
+    tp.jmap_lo[v] = (uint16_t)swz(jlo);
+    tp.jmap_hi[v] = (uint16_t)swz(jhi);
+  }
+  tp.nchunks = (nbits + 7) / 8;
+  for (int c = 0; c < tp.nchunks; ++c)
+    for (int v = 0; v < 256; ++v) {
+      uint64_t p = 0;
+      for (int j = 0; j < 8; ++j) {
+        const int k = 8 * c + j;
+        if (k < nbits && ((v >> j) & 1)) p |= uint64_t(1) << perm[k];
+      }
+      tp.plut[c * 256 + v] = p;
+    }
+  return true;
+}
+
+int launch_tperm(const double2* src, double2* dst, int nbits, const TilePerm& tp, cudaStream_t st) {
+  const uint64_t ntiles = uint64_t(1) << (nbits - tp.nt);
+  const size_t smem = sizeof(double2) << tp.nt;
+  uint64_t grid = (uint64_t)num_sms() * 6;
+  if (grid > ntiles) grid = ntiles;
+  k_tperm<<<(unsigned)grid, kTileThreads, smem, st>>>(src, dst, tp, ntiles);
+  SVB_CHECK_LAUNCH("tiled bit permutation");
+  return SVB_OK;
+}
+
+// dst[t] = src[P(base + t)], t < count (P from 8-bit lookup tables): one
+// contiguous chunk of a permuted order, e.g. basis-sorted shard order for
+// the chunked gather
+__global__ void k_gather_bits(const double2* __restrict__ src, double2* __restrict__ dst, int nbits,
+                              const __grid_constant__ PermLut lut_p, uint64_t base, uint64_t count) {
+  __shared__ uint64_t lut[5 * 256];
+  const int nchunks = (nbits + 7) / 8;
+  for (int i = threadIdx.x; i < nchunks * 256; i += blockDim.x) lut[i] = lut_p.v[i];
+  __syncthreads();
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < count; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t f = base + t;
+    uint64_t p = 0;
+    for (int c = 0; c < nchunks; ++c) p |= lut[c * 256 + ((f >> (8 * c)) & 255)];
+    dst[t] = src[p];
+  }
+}
+
 int grid_for(uint64_t work, int threads) {
   uint64_t b = (work + threads - 1) / threads;
   const uint64_t cap = (uint64_t)num_sms() * 32;
@@ -171,6 +370,18 @@ extern "C" int svb_bitswap(svb_c128* state, int D, const int32_t* u, const int32
   bs.nrest = 0;
   for (int b = 0; b < D; ++b)
     if (!(used >> b & 1)) bs.rest[bs.nrest++] = b;
+  {  // tiled in place when the swapped bits and the low bits fit one tile
+    int32_t perm[64];
+    for (int b = 0; b < D; ++b) perm[b] = b;
+    for (int i = 0; i < m; ++i) {
+      perm[u[i]] = w[i];
+      perm[w[i]] = u[i];
+    }
+    static thread_local TilePerm tp;  // host-side parameter block (about 13 KB)
+    if (D >= kTileBits && make_tile_perm(D, perm, true, tp))
+      return launch_tperm(reinterpret_cast<const double2*>(state), reinterpret_cast<double2*>(state), D, tp,
+                          as_stream(stream));
+  }
   const uint64_t total = uint64_t(1) << D;  // (2^(D-2m) bases) x (4^m combos)
   k_bitswap<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<double2*>(state), bs, total);
@@ -227,6 +438,12 @@ extern "C" int svb_bitperm(const svb_c128* src, svb_c128* dst, int nbits, const 
     }
     used |= uint64_t(1) << perm[k];
   }
+  {
+    static thread_local TilePerm tp;
+    if (nbits >= kTileBits && make_tile_perm(nbits, perm, false, tp))
+      return launch_tperm(reinterpret_cast<const double2*>(src), reinterpret_cast<double2*>(dst), nbits, tp,
+                          as_stream(stream));
+  }
   PermLut lut;
   const int nchunks = (nbits + 7) / 8;
   for (int c = 0; c < nchunks; ++c)
@@ -242,5 +459,38 @@ extern "C" int svb_bitperm(const svb_c128* src, svb_c128* dst, int nbits, const 
   k_bitperm<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<const double2*>(src), reinterpret_cast<double2*>(dst), nbits, lut, total);
   SVB_CHECK_LAUNCH("svb_bitperm");
+  return SVB_OK;
+}
+
+// dst[t] = src[P(base + t)] for t < count, P(f) = sum_k bit_k(f) << perm[k]
+extern "C" int svb_gather_bits(const svb_c128* src, int nbits, const int32_t* perm, uint64_t base, int64_t count,
+                               svb_c128* dst, void* stream) {
+  if (nbits < 0 || nbits > 40 || count < 0) {
+    set_error("gather_bits: bad arguments (nbits=%d)", nbits);
+    return SVB_ERANGE;
+  }
+  uint64_t used = 0;
+  for (int k = 0; k < nbits; ++k) {
+    if (perm[k] < 0 || perm[k] >= nbits || (used >> perm[k] & 1)) {
+      set_error("gather_bits: not a permutation");
+      return SVB_EINVAL;
+    }
+    used |= uint64_t(1) << perm[k];
+  }
+  if (count == 0) return SVB_OK;
+  PermLut lut;
+  const int nchunks = (nbits + 7) / 8;
+  for (int c = 0; c < nchunks; ++c)
+    for (int v = 0; v < 256; ++v) {
+      uint64_t p = 0;
+      for (int j = 0; j < 8; ++j) {
+        const int k = 8 * c + j;
+        if (k < nbits && ((v >> j) & 1)) p |= uint64_t(1) << perm[k];
+      }
+      lut.v[c * 256 + v] = p;
+    }
+  k_gather_bits<<<grid_for((uint64_t)count, 256), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const double2*>(src), reinterpret_cast<double2*>(dst), nbits, lut, base, (uint64_t)count);
+  SVB_CHECK_LAUNCH("svb_gather_bits");
   return SVB_OK;
 }

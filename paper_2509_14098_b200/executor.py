@@ -1066,9 +1066,73 @@ def gather_device(state: DistState) -> torch.Tensor:
     return dense
 
 
-def gather(state: DistState) -> np.ndarray:
-    """Dense host vector, like the reference's gather (executor.py:320-326)."""
-    return gather_device(state).cpu().numpy()
+GATHER_CHUNK_BITS = int(os.environ.get("SVB200_GATHER_CHUNK_BITS", "22"))  # 64 MiB chunks
+
+
+def gather(state: DistState, root: int | None = None) -> np.ndarray | None:
+    """Dense host vector, like the reference's gather (executor.py:320-326).
+
+    A sharded state is assembled chunk by chunk in host memory: every
+    process reads its shard in basis-sorted order one 2^22-amplitude chunk
+    at a time (svb_gather_bits), the chunks are all-gathered (gathered to
+    `root` when given) and written into the dense vector through a strided
+    view, so no GPU ever holds more than its shard plus world chunks.  With
+    root, processes other than root return None.  One large single-GPU
+    state takes the same chunked path (no second full-size device buffer)."""
+    big = (16 << state.d) > (1 << 33)  # > 8 GiB: avoid a full-size device copy
+    if state.world == 1 and not big:
+        return gather_device(state).cpu().numpy()
+    return _gather_chunked(state, root)
+
+
+@_on_device(lambda state, *a, **k: _arg_device(state))
+def _gather_chunked(state: DistState, root: int | None) -> np.ndarray | None:
+    import torch.distributed as dist
+
+    from . import sampling
+
+    lib = _native.load()
+    d, g, world = state.d, state.g, state.world
+    blocks = state.blocks.contiguous()
+    rows = blocks.shape[0]
+    layout = state.layouts[state.phase]
+    me = state.rank_base // rows
+    want = root is None or root == me
+    dense = np.empty(1 << d, dtype=np.complex128) if want else None
+    view = dense.reshape((2,) * d) if want and d else dense
+    geos = [sampling.shard_geometry(layout, d, g, rows, p * rows) for p in range(world)]
+    D, perm, _, _ = geos[me]
+    inv = [0] * D  # sorted bit -> storage bit
+    for s_, j in enumerate(perm):
+        inv[j] = s_
+    arr, inv32 = _native.i32_array(inv)
+    c = min(D, GATHER_CHUNK_BITS)
+    stage = torch.empty(1 << c, dtype=torch.complex128, device=blocks.device)
+    bufs = [torch.empty_like(stage) for _ in range(world)] if world > 1 else [stage]
+    stream = _stream_ptr(blocks.device)
+
+    def place(p, k, host):
+        Dp, _, fm, fv = geos[p]
+        idx = []
+        for axis in range(d):  # axis 0 = basis bit d-1 (qubit 0)
+            bit = d - 1 - axis
+            idx.append(((fv >> bit) & 1) if (fm >> bit) & 1 else slice(None))
+        sub = view[tuple(idx)] if d else view
+        lead = tuple((k >> (Dp - c - 1 - i)) & 1 for i in range(Dp - c))
+        sub[lead] = host.reshape((2,) * c) if c else host
+
+    for k in range(1 << (D - c)):
+        _native.check(lib.svb_gather_bits(blocks.data_ptr(), D, inv32, k << c, 1 << c, stage.data_ptr(), stream),
+                      "svb_gather_bits")
+        if world > 1:
+            if root is None or dist.get_backend(state.group) == "gloo":
+                dist.all_gather(bufs, stage, group=state.group)
+            else:
+                dist.gather(stage, bufs if want else None, dst=root, group=state.group)
+        if want:
+            for p in range(world):
+                place(p, k, bufs[p].cpu().numpy())
+    return dense
 
 
 @_on_device(lambda dense, plan, phase=0, device=None, **k: device or _arg_device(dense))

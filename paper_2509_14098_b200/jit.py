@@ -536,9 +536,9 @@ GROUPS_MIN_DFMA = float(os.environ.get("SVB200_JIT_GROUPS_MIN_DFMA", "48"))
 
 
 def dfma_per_amp(ops, rb: int) -> float:
-    """Rough FP64 FMA count per amplitude of a sweep's op list: a 4x4 on
-    register pairs 16, a 2x2 8, an H 1, phases ~4 (bookkeeping for the
-    tile-group choice, not the roofline)."""
+    """FP64 FMAs per amplitude of a sweep's dense gates: a 4x4 on register
+    pairs 16, a 2x2 8 (the tile-group choice; phase-only sweeps stay in one
+    group, measured faster on the QFT; the roofline counts SASS instead)."""
     n = 0.0
     for op in ops:
         k = int(op["kind"])
@@ -546,10 +546,6 @@ def dfma_per_amp(ops, rb: int) -> float:
             n += 16
         elif k == prog.OP_U1:
             n += 8
-        elif k == prog.OP_H:
-            n += 1 + (4 if int(op["flags"]) & prog.F_PHASE else 0)
-        elif k in (prog.OP_PH, prog.OP_PHALL):
-            n += 4
     return n
 
 
