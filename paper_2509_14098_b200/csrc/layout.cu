@@ -110,53 +110,63 @@ __global__ void k_bitperm(const double2* __restrict__ src, double2* __restrict__
 // order; the XOR swizzle keeps both access patterns conflict free.  With
 // src == dst the permutation must map every tile onto itself (bit swaps
 // whose bits are all tile bits): the swap is then in place.
-constexpr int kTileBits = 10;
+constexpr int kTileBits = 11;
 constexpr int kTileThreads = 256;
 
 struct TilePerm {
   int nt;                        // tile bits
   int nrest;                     // non-tile source bits (tile index), ascending
   int rest[SVB_MAX_DEV_BITS];
-  uint64_t ld_lo[32], ld_hi[32];  // load-order index -> source offset bits
-  uint64_t st_lo[32], st_hi[32];  // store-order index -> destination offset bits
-  uint16_t jmap_lo[32], jmap_hi[32];  // store-order index -> swizzled smem slot
-  uint32_t swz_lo[32], swz_hi[32];    // load-order index -> swizzled smem slot
-  int nchunks;
-  uint64_t plut[5 * 256];        // P on source indices (tile bases)
+  int rest_dst[SVB_MAX_DEV_BITS];  // perm[rest[i]]
+  uint64_t ld_lo[64], ld_hi[32];  // load-order index (low 6 / high 5 bits) -> source offset bits
+  uint64_t st_lo[64], st_hi[32];  // store-order index -> destination offset bits
+  uint16_t jmap_lo[64], jmap_hi[32];  // store-order index -> swizzled smem slot
+  uint32_t swz_lo[64], swz_hi[32];    // load-order index -> swizzled smem slot
 };
 
 __global__ void __launch_bounds__(kTileThreads) k_tperm(const double2* __restrict__ src, double2* __restrict__ dst,
                                                         const __grid_constant__ TilePerm tp, uint64_t ntiles) {
   extern __shared__ __align__(16) double2 tile[];
-  __shared__ uint64_t plut[5 * 256];
   // per-lane table lookups from shared memory (parameter-space reads with
   // lane-varying indices would serialise in the constant cache)
-  __shared__ uint64_t ld_lo[32], ld_hi[32], st_lo[32], st_hi[32];
-  __shared__ uint32_t sw_lo[32], sw_hi[32], jm_lo[32], jm_hi[32];
-  for (int i = threadIdx.x; i < tp.nchunks * 256; i += blockDim.x) plut[i] = tp.plut[i];
-  if (threadIdx.x < 32) {
+  __shared__ uint64_t ld_lo[64], ld_hi[32], st_lo[64], st_hi[32];
+  __shared__ uint32_t sw_lo[64], sw_hi[32], jm_lo[64], jm_hi[32];
+  const int lane = threadIdx.x & 31;
+  // tile bases: lane l deposits non-tile bit l of the tile index (source and
+  // destination position), OR-reduced over the warp
+  const int rest_src = lane < tp.nrest ? tp.rest[lane] : 0;
+  const int rest_dst = lane < tp.nrest ? tp.rest_dst[lane] : 0;
+  if (threadIdx.x < 64) {
     const int v = threadIdx.x;
     ld_lo[v] = tp.ld_lo[v];
-    ld_hi[v] = tp.ld_hi[v];
     st_lo[v] = tp.st_lo[v];
-    st_hi[v] = tp.st_hi[v];
     sw_lo[v] = tp.swz_lo[v];
-    sw_hi[v] = tp.swz_hi[v];
     jm_lo[v] = tp.jmap_lo[v];
+  }
+  if (threadIdx.x < 32) {
+    const int v = threadIdx.x;
+    ld_hi[v] = tp.ld_hi[v];
+    st_hi[v] = tp.st_hi[v];
+    sw_hi[v] = tp.swz_hi[v];
     jm_hi[v] = tp.jmap_hi[v];
   }
   __syncthreads();
   const int n = 1 << tp.nt;
   for (uint64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-    uint64_t sb = 0;
-    for (int i = 0; i < tp.nrest; ++i) sb |= ((ti >> i) & 1ull) << tp.rest[i];
-    uint64_t db = 0;
-    for (int c = 0; c < tp.nchunks; ++c) db |= plut[c * 256 + ((sb >> (8 * c)) & 255)];
+    const uint64_t on = lane < tp.nrest ? (ti >> lane) & 1ull : 0ull;
+    uint64_t sb = on << rest_src, db = on << rest_dst;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      sb |= __shfl_xor_sync(0xffffffffu, sb, o);
+      db |= __shfl_xor_sync(0xffffffffu, db, o);
+    }
+#pragma unroll 8
     for (int j = threadIdx.x; j < n; j += blockDim.x)
-      tile[sw_lo[j & 31] ^ sw_hi[j >> 5]] = src[sb | ld_lo[j & 31] | ld_hi[j >> 5]];
+      tile[sw_lo[j & 63] ^ sw_hi[j >> 6]] = src[sb | ld_lo[j & 63] | ld_hi[j >> 6]];
     __syncthreads();
+#pragma unroll 8
     for (int k = threadIdx.x; k < n; k += blockDim.x)
-      st_stream(dst + (db | st_lo[k & 31] | st_hi[k >> 5]), tile[jm_lo[k & 31] ^ jm_hi[k >> 5]]);
+      st_stream(dst + (db | st_lo[k & 63] | st_hi[k >> 6]), tile[jm_lo[k & 63] ^ jm_hi[k >> 6]]);
     __syncthreads();
   }
 }
@@ -207,7 +217,11 @@ bool make_tile_perm(int nbits, const int32_t* perm, bool inplace, TilePerm& tp) 
   tp.nt = nt;
   tp.nrest = 0;
   for (int b = 0; b < nbits; ++b)
-    if (!in_t[b]) tp.rest[tp.nrest++] = b;
+    if (!in_t[b]) {
+      tp.rest_dst[tp.nrest] = perm[b];
+      tp.rest[tp.nrest++] = b;
+    }
+  if (tp.nrest > 32) return false;  // one warp lane per non-tile bit
   // load-order position of each store-order bit
   int pos_of_src[64];
   for (int i = 0; i < nt; ++i) pos_of_src[src_t[i]] = i;
@@ -233,50 +247,43 @@ bool make_tile_perm(int nbits, const int32_t* perm, bool inplace, TilePerm& tp) 
     for (int f = 0; f < nf; ++f) x ^= ((j >> fold_from[f]) & 1u) << fold_to[f];
     return x;
   };
-  for (int v = 0; v < 32; ++v) {
-    uint64_t llo = 0, lhi = 0, slo = 0, shi = 0;
-    uint32_t jlo = 0, jhi = 0;
-    for (int i = 0; i < 5; ++i) {
+  // index tables split into the low 6 and high 5 index bits; the swizzle is
+  // linear over XOR, so slot(j) = slot(j & 63) ^ slot(j & ~63)
+  for (int v = 0; v < 64; ++v) {
+    uint64_t llo = 0, slo = 0;
+    uint32_t jlo = 0;
+    for (int i = 0; i < 6 && i < nt; ++i)
       if ((v >> i) & 1) {
-        if (i < nt) {
-          llo |= uint64_t(1) << src_t[i];
-          slo |= uint64_t(1) << dst_t[i];
-          jlo |= 1u << jpos[i];
-        }
-        if (i + 5 < nt) {
-          lhi |= uint64_t(1) << src_t[i + 5];
-          shi |= uint64_t(1) << dst_t[i + 5];
-          jhi |= 1u << jpos[i + 5];
-        }
+        llo |= uint64_t(1) << src_t[i];
+        slo |= uint64_t(1) << dst_t[i];
+        jlo |= 1u << jpos[i];
       }
-    }
     tp.ld_lo[v] = llo;
-    tp.ld_hi[v] = lhi;
     tp.st_lo[v] = slo;
-    tp.st_hi[v] = shi;
-    // swizzle is linear (XOR of bit images): split over the two halves
-    tp.swz_lo[v] = swz((uint32_t)v);  // linear over XOR: slot(j) = slot(j & 31) ^ slot(j & ~31)
-    tp.swz_hi[v] = swz((uint32_t)v << 5);
+    tp.swz_lo[v] = swz((uint32_t)v);
     tp.jmap_lo[v] = (uint16_t)swz(jlo);
+  }
+  for (int v = 0; v < 32; ++v) {
+    uint64_t lhi = 0, shi = 0;
+    uint32_t jhi = 0;
+    for (int i = 0; i < 5 && i + 6 < nt; ++i)
+      if ((v >> i) & 1) {
+        lhi |= uint64_t(1) << src_t[i + 6];
+        shi |= uint64_t(1) << dst_t[i + 6];
+        jhi |= 1u << jpos[i + 6];
+      }
+    tp.ld_hi[v] = lhi;
+    tp.st_hi[v] = shi;
+    tp.swz_hi[v] = swz((uint32_t)v << 6);
     tp.jmap_hi[v] = (uint16_t)swz(jhi);
   }
-  tp.nchunks = (nbits + 7) / 8;
-  for (int c = 0; c < tp.nchunks; ++c)
-    for (int v = 0; v < 256; ++v) {
-      uint64_t p = 0;
-      for (int j = 0; j < 8; ++j) {
-        const int k = 8 * c + j;
-        if (k < nbits && ((v >> j) & 1)) p |= uint64_t(1) << perm[k];
-      }
-      tp.plut[c * 256 + v] = p;
-    }
   return true;
 }
 
 int launch_tperm(const double2* src, double2* dst, int nbits, const TilePerm& tp, cudaStream_t st) {
   const uint64_t ntiles = uint64_t(1) << (nbits - tp.nt);
   const size_t smem = sizeof(double2) << tp.nt;
-  uint64_t grid = (uint64_t)num_sms() * 6;
+  uint64_t grid = (uint64_t)num_sms() * 6;  // 32 KB tiles: six CTAs per SM
   if (grid > ntiles) grid = ntiles;
   k_tperm<<<(unsigned)grid, kTileThreads, smem, st>>>(src, dst, tp, ntiles);
   SVB_CHECK_LAUNCH("tiled bit permutation");

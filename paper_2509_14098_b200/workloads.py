@@ -197,6 +197,14 @@ def _inverse_line(line: str) -> str:
     raise ValueError(f"no inverse for {name}")
 
 
+def inverse(qasm: str) -> str:
+    """U^dagger of a circuit: its gates inverted in reverse order."""
+    lines = qasm.strip().splitlines()
+    head = [ln for ln in lines if ln.startswith(("OPENQASM", "include", "qreg"))]
+    body = [ln for ln in lines if ln not in head and ln.strip()]
+    return "\n".join(head + [_inverse_line(ln) for ln in reversed(body)]) + "\n"
+
+
 def mirror(qasm: str) -> str:
     """U followed by U^dagger: the exact output is |0...0> (a full-size known answer)."""
     lines = qasm.strip().splitlines()

@@ -263,6 +263,8 @@ BENCH = [
     ("mirror_qv31_h29-12", lambda: workloads.mirror(workloads.quantum_volume(31, seed=10, depth=12)), [29, 12]),
     ("mirror_sup31_h29-12", lambda: workloads.mirror(workloads.random_supremacy(31, seed=11)), [29, 12]),
     ("mirror_qaoa31_h29-12", lambda: workloads.mirror(workloads.qaoa_maxcut(31, seed=12, p=2)), [29, 12]),
+    # the exact QV-30 bench circuit inverted: forward + inverse from a random basis state on one GPU
+    ("qv30inv_h30-12", lambda: workloads.inverse(workloads.quantum_volume(30, seed=34)), [30, 12]),
     # 34-qubit QV mirror on 2 GPUs (cfg3 shape, half depth each way): tools/dist_check.py --qv34
     ("mirror_qv34_h33-12", lambda: workloads.mirror(workloads.quantum_volume(34, seed=13, depth=17)), [33, 12]),
 ]

@@ -243,7 +243,7 @@ def test_compare_propagates_nan():
     assert compare(a, a) == 0.0
 
 
-@pytest.mark.parametrize("nbits", [10, 13, 17, 22])
+@pytest.mark.parametrize("nbits", [10, 11, 12, 13, 17, 22])
 def test_layout_kernels_match_numpy(nbits):
     """svb_bitperm (tiled when a tile of <= 10 bits covers the low source
     and destination bits) and in-place svb_bitswap against numpy index math."""

@@ -47,17 +47,100 @@ def test_mirror_circuits_return_to_zero(name):
     assert b.abs().max().item() < 1e-10
 
 
-def test_qft30_bench_plan_norm_and_layout():
-    """The bench workload itself: norm preserved after every leaf (drift check) and the
-    amplitude of |0> after QFT|0> is exactly uniform."""
+def _basis_blocks(plan, x):
+    """Rank blocks (phase-0 layout) of the basis state |x> on the device."""
+    d, g = plan.d, plan.g
+    L = d - g
+    f = 0
+    for q in range(d):
+        if (x >> (d - 1 - q)) & 1:
+            f |= 1 << (d - 1 - plan.layout_phases[0][q])
+    init = torch.zeros((1 << g, 1 << L), dtype=torch.complex128, device="cuda")
+    init[f >> L, f & ((1 << L) - 1)] = 1.0
+    return init, f
+
+
+def _storage_index(layout, d, x):
+    f = 0
+    for q in range(d):
+        if (x >> (d - 1 - q)) & 1:
+            f |= 1 << (d - 1 - layout[q])
+    return f
+
+
+def _closed_form_err(state, x):
+    d = state.d
+    layout = state.layouts[state.phase]
+    flat = state.blocks.reshape(-1)
+    mask = (1 << d) - 1
+    err = 0.0
+    for off in range(0, flat.numel(), 1 << 25):
+        idx = torch.arange(off, min(off + (1 << 25), flat.numel()), device=flat.device, dtype=torch.int64)
+        y = torch.zeros_like(idx)
+        for q in range(d):
+            y |= ((idx >> (d - 1 - layout[q])) & 1) << (d - 1 - q)
+        r = ((y * (x & 0xFFFFF)) + (((y * (x >> 20)) & ((1 << (d - 20)) - 1)) << 20)) & mask
+        exp = torch.exp(-2j * np.pi * r.to(torch.float64) / (1 << d)) / 2 ** (d / 2)
+        err = max(err, (flat[off:off + idx.numel()] - exp).abs().max().item())
+    return err
+
+
+def test_qft30_bench_plan_closed_form():
+    """The exact bench plan (cfg2) on a random basis state |x> against the
+    closed form: every amplitude and its storage position are checked, so a
+    wrong layout, relabel or materialisation shows (QFT|0> is uniform and
+    would hide it); |0...0> itself is checked too (the sparse-start path)."""
     from paper_2509_14098_b200 import run_plan
 
     plan = load("qft30_h30-12")
-    res = run_plan(plan)
-    b = res.state.blocks.reshape(-1)
-    amp = 2 ** -15
-    assert (b - amp).abs().max().item() < 1e-12
+    x = 0x2B3C5D17 & ((1 << 30) - 1)
+    init, _ = _basis_blocks(plan, x)
+    res = run_plan(plan, initial=init)
+    del init
+    assert _closed_form_err(res.state, x) < 1e-10
+    del res
+    res = run_plan(plan)  # |0...0>: sparse support-only sweeps
     assert res.stats.sweeps == 4
+    assert _closed_form_err(res.state, 0) < 1e-12
+
+
+def test_qv30_bench_plan_forward_and_inverse():
+    """The exact QV-30 bench plan (cfg3's family on one GPU), then the plan
+    of its inverse circuit, from a random basis state: the result must be
+    that basis state, amplitude and position."""
+    from paper_2509_14098_b200 import run_plan
+
+    fwd, inv = load("qv30_h30-12"), load("qv30inv_h30-12")
+    x = 0x1D2C3B4A & ((1 << 30) - 1)
+    init, f = _basis_blocks(fwd, x)
+    res = run_plan(fwd, initial=init)
+    del init
+    assert fwd.layout_phases[-1] == inv.layout_phases[0]  # one rank: the identity layout
+    back = run_plan(inv, initial=res.state.blocks)
+    del res
+    b = back.state.blocks.reshape(-1)
+    fx = _storage_index(inv.layout_phases[-1], 30, x)
+    assert abs(b[fx].item() - 1.0) < 1e-10
+    b[fx] = 0
+    assert b.abs().max().item() < 1e-10
+
+
+@pytest.mark.parametrize("name", ["mirror_qv24_h22-12", "mirror_qaoa24_h24-12", "mirror_sup24_h21-12",
+                                  "mirror_qv28_h28-12"])
+def test_mirror_circuits_from_basis_state(name):
+    """U U^dagger from a random basis state |x> returns |x> at its storage
+    position (from |0...0> a wrong permutation would go unnoticed)."""
+    from paper_2509_14098_b200 import run_plan
+
+    plan = load(name)
+    x = int(np.random.default_rng(plan.d).integers(1, 1 << plan.d))
+    init, _ = _basis_blocks(plan, x)
+    res = run_plan(plan, initial=init)
+    b = res.state.blocks.reshape(-1)
+    fx = _storage_index(plan.layout_phases[-1], plan.d, x)
+    assert abs(b[fx].item() - 1.0) < 1e-10, name
+    b[fx] = 0
+    assert b.abs().max().item() < 1e-10, name
 
 
 def test_coresident_ranks_closed_form_qft31():
