@@ -215,9 +215,15 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
         return hit[1]
     t0 = time.perf_counter()
     dist_run = _dist_info()[1] > 1
-    dp = prog.plan_device(plan, geo, rb=JIT_REG_BITS if use_jit else prog.RB,
-                          overlap_bits=_overlap_bits() if (use_jit and dist_run) else 0,
-                          free_start=zero_start, stable_threads=use_jit and jitmod_shuffle())
+    ob = _overlap_bits() if (use_jit and dist_run) else 0
+    skip_first = False
+    if ob and zero_start and SPARSE_START:
+        dp0 = prog.plan_device(plan, geo, rb=JIT_REG_BITS, overlap_bits=0, free_start=True,
+                               stable_threads=jitmod_shuffle())
+        skip_first = prog.sparse_reaches_first_remap(dp0, geo.D)
+    dp = prog.plan_device(plan, geo, rb=JIT_REG_BITS if use_jit else prog.RB, overlap_bits=ob,
+                          free_start=zero_start, stable_threads=use_jit and jitmod_shuffle(),
+                          overlap_skip_first=skip_first)
     blob, descs, _ = prog.pack(dp.buf)
     host = np.ascontiguousarray(blob)
     dev_blob = torch.from_numpy(host).to(device)

@@ -682,7 +682,8 @@ MAX_CHAIN = int(os.environ.get("SVB200_MAX_CHAIN", "3"))  # sweeps before a rema
 MIN_OVERLAP_BIT = 8
 
 
-def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int, max_chain: int = MAX_CHAIN) -> None:
+def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int, max_chain: int = MAX_CHAIN,
+                  skip_first: bool = False) -> None:
     """Chunk bits for remaps whose neighbouring sweeps can run in parts.
 
     The chunk bits lie outside the tiles of the sweep after the remap, of a
@@ -692,9 +693,14 @@ def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int, max_chain: 
     if nbits <= 0:
         return
     L = geo.L + geo.h  # planner-owned bits (local + rows of this device)
+    first_seen = False
     for i, st in enumerate(steps):
         if st.kind != "exchange" or not st.swaps:
             continue
+        if skip_first and not first_seen:  # its sweeps run sparse (sparse_start) instead
+            first_seen = True
+            continue
+        first_seen = True
         if any(ib < geo.h for ib, _ in st.swaps):
             continue  # part of the remap is an in-HBM bit swap over all chunks
         if min(lb for _, lb in st.swaps) < MIN_OVERLAP_BIT:
@@ -746,7 +752,8 @@ def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int, max_chain: 
 
 def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_BITS,
                 max_materialize: int = 64, rb: int = RB, fuse: bool = True,
-                overlap_bits: int = 0, free_start: bool = True, stable_threads: bool = False) -> DeviceProgram:
+                overlap_bits: int = 0, free_start: bool = True, stable_threads: bool = False,
+                overlap_skip_first: bool = False) -> DeviceProgram:
     """Compile every ApplyFused task of a plan for one device, with a global layout.
 
     The physical layout is a permutation `where` of the local bits that the
@@ -968,7 +975,7 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
         run_segment(seg)
     slot = len(task_slot)
 
-    _plan_overlap(steps, buf, geo, overlap_bits)
+    _plan_overlap(steps, buf, geo, overlap_bits, skip_first=overlap_skip_first)
 
     # restore the reference layout
     first = len(buf.descs)
@@ -1050,6 +1057,23 @@ def sparse_start(dp: "DeviceProgram", D: int, unit: bool) -> dict:
     if s0 == 0 and not any(int(o["kind"]) == OP_STAGE for o in ops):
         return {}
     return {i: (s, k == len(seq) - 1) for k, (i, s) in enumerate(seq)}
+
+
+def sparse_reaches_first_remap(dp: "DeviceProgram", D: int) -> bool:
+    """True when, from |0...0> on the device holding the unit vector, every
+    sweep before the first data-moving remap is sparse (its support never
+    covers the device): those sweeps then cost a fraction of a pass, and
+    running them in overlapped parts (which keeps them dense) would be
+    slower than the remap they hide behind.  Decided on a program planned
+    without overlap, identically on every process."""
+    sp = sparse_start(dp, D, True)
+    for st in dp.steps:
+        if st.kind == "exchange" and st.swaps:
+            return True
+        if st.kind in ("sweeps", "materialize"):
+            if any(i not in sp for i in range(st.first, st.first + st.count)):
+                return False
+    return False
 
 
 def sparse_bytes(desc: dict, sparse) -> tuple:
