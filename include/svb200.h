@@ -193,15 +193,7 @@ int svb_shard_argmax(const svb_c128* a, const svb_c128* b, int64_t n, uint64_t b
 int svb_shard_maxdev(const svb_c128* a, const svb_c128* b, int64_t n, double phi_re, double phi_im,
                      double* out, void* scratch, void* stream);
 
-/* Device sampling (executor.py:375-383; paper_2509_14098_b200/sampling.py).
- * svb_probs_sorted: out[perm(t)] = |shard[t]|^2 for the 2^D shard elements,
- *   perm[s] = sorted-order bit of shard bit s (basis-sorted shard order).
- * svb_sample_prefix: out[s] = cdf[c - 1] (0 if c = 0) where c = number of
- *   shard elements with basis index <= mid[s]; the shard's basis indices
- *   have fixed_val at the fixed_mask bits and run over the other d bits. */
-int svb_probs_sorted(const svb_c128* shard, int D, const int32_t* perm, double* out, void* stream);
-int svb_sample_prefix(const double* cdf, int d, uint64_t fixed_mask, uint64_t fixed_val,
-                      const int64_t* mid, int64_t nshots, double* out, void* stream);
+/* Device sampling: section 7 (numpy-identical CDF). */
 
 /* ------------------------------------------------------------------------
  * 5. Run-time specialised sweep kernels (paper_2509_14098_b200/jit.py).

@@ -20,7 +20,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 LIB = PKG / "libsvb200.so"
-SOURCES = ["gate_kernels.cu", "sweep.cu", "layout.cu", "reduce.cu", "jit.cu", "peer.cu", "sample.cu", "cdf.cu"]
+SOURCES = ["gate_kernels.cu", "sweep.cu", "layout.cu", "reduce.cu", "jit.cu", "peer.cu", "cdf.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -42,8 +42,6 @@ _SIGS = {
     "svb_shard_scratch_bytes": ([_i64], _sz),
     "svb_shard_argmax": ([_vp, _vp, _i64, _c.c_uint64, _int, _pi32, _vp, _vp, _vp], _int),
     "svb_shard_maxdev": ([_vp, _vp, _i64, _c.c_double, _c.c_double, _vp, _vp, _vp], _int),
-    "svb_probs_sorted": ([_vp, _int, _pi32, _vp, _vp], _int),
-    "svb_sample_prefix": ([_vp, _int, _c.c_uint64, _c.c_uint64, _vp, _i64, _vp, _vp], _int),
     "svb_jit_compile": ([_c.c_char_p, _c.c_char_p, _int, _c.POINTER(_c.c_char_p), _c.POINTER(_vp),
                          _c.POINTER(_sz), _c.c_char_p, _sz], _int),
     "svb_jit_free": ([_vp], None),
