@@ -270,9 +270,10 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
 
 
 def jitmod_shuffle() -> bool:
+    """Planner-chosen stable thread-bit orders (warp-local stage changes)."""
     from . import jit as jitmod
 
-    return jitmod.SHUFFLE_STAGES
+    return jitmod.SHUFFLE_STAGES or jitmod.LOCAL_STAGES
 
 
 def _has_remote(st, geo) -> bool:

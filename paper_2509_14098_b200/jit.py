@@ -53,12 +53,13 @@ def _lit_raw(x: float) -> str:
     return r if ("e" in r or "." in r or "inf" in r or "nan" in r) else r + ".0"
 
 
-# Coefficients of the kernel being generated go to a __constant__ table: a
-# DFMA then reads its literal straight from the constant bank, whereas FP64
-# immediates would be materialised with two UMOVs each (ncu round 2: 1,395
-# UMOVs beside 3,184 DFMAs per tile of the heaviest QV sweep)
+# Coefficients of the kernel being generated can go to a __constant__ table
+# (SVB200_JIT_CONST_POOL=1): FP64 literals are otherwise materialised with
+# two UMOVs each (ncu round 2: 1,395 UMOVs beside 3,184 DFMAs per tile of the
+# heaviest QV sweep).  Measured on B200: the table's uniform-register loads
+# raise register pressure into spills and QV-30 ran 667 -> 731 ms, so it is off
 _POOL: dict | None = None
-CONST_POOL = os.environ.get("SVB200_JIT_CONST_POOL", "1") not in ("0", "false", "no")
+CONST_POOL = os.environ.get("SVB200_JIT_CONST_POOL", "0") not in ("0", "false", "no")
 _INLINE = {0.0, 1.0, -1.0, 0.5, -0.5, 2.0, -2.0}
 
 
@@ -142,6 +143,19 @@ def _xor_img(var: str, imgs) -> str:
 # ---------------------------------------------------------------------------
 # kernel generator
 # ---------------------------------------------------------------------------
+
+# stage changes that keep the warp-level thread bits (thread bits 5..) on the
+# same tile bits move data only within each warp: a __syncwarp replaces the
+# CTA barrier, so warps no longer meet at every stage (planner-chosen stable
+# thread-bit orders make most QV stage changes warp-local)
+LOCAL_STAGES = os.environ.get("SVB200_JIT_LOCAL_STAGES", "1") not in ("0", "false", "no")
+
+
+def _warp_local_change(stage_info: list, a: int, b: int, nthreads: int) -> bool:
+    if not LOCAL_STAGES or nthreads < 64:
+        return False
+    return list(stage_info[a][1][5:]) == list(stage_info[b][1][5:])
+
 
 def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int = 0,
                   sparse: tuple | None = None) -> str:
@@ -496,7 +510,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                     for v in range(NR):
                         if hf is None or ((v >> q) & 1) == hf[1]:
                             w(f"    tile[sb{cur} ^ {offs[v]}u] = x[{v}];")
-                w("    __syncthreads();")
+                w("    __syncwarp();" if _warp_local_change(stage_info, cur, nxt, NT) else "    __syncthreads();")
             else:
                 flush()
             pending = []
@@ -771,7 +785,10 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
                 _, _, offs = stage_info[cur]
                 for v in range(NR):
                     w(f"    tile[sb{cur} ^ {offs[v]}u] = x[{v}];")
-                w(f"    bar_group(bar_id, {NT}u);")
+                if _warp_local_change(stage_info, cur, nxt, NT):
+                    w("    __syncwarp();")
+                else:
+                    w(f"    bar_group(bar_id, {NT}u);")
             _, _, offs = stage_info[nxt]
             if nxt == 0 and zero_init:
                 for v in range(NR):
