@@ -145,10 +145,12 @@ def _xor_img(var: str, imgs) -> str:
 # ---------------------------------------------------------------------------
 
 # stage changes that keep the warp-level thread bits (thread bits 5..) on the
-# same tile bits move data only within each warp: a __syncwarp replaces the
-# CTA barrier, so warps no longer meet at every stage (planner-chosen stable
-# thread-bit orders make most QV stage changes warp-local)
-LOCAL_STAGES = os.environ.get("SVB200_JIT_LOCAL_STAGES", "1") not in ("0", "false", "no")
+# same tile bits move data only within each warp: a __syncwarp can replace
+# the CTA barrier (planner-chosen stable thread-bit orders make 86 of QV-30's
+# 163 stage changes warp-local).  Measured on B200: correct, but QV-30 ran
+# 669 -> 691 ms (warps that drift apart in a ~200 KB straight-line kernel
+# share fewer instruction fetches), so it is off by default
+LOCAL_STAGES = os.environ.get("SVB200_JIT_LOCAL_STAGES", "0") not in ("0", "false", "no")
 
 
 def _warp_local_change(stage_info: list, a: int, b: int, nthreads: int) -> bool:
@@ -265,6 +267,30 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                     o ^= sw[regs[q]]
             offs.append(o)
         stage_info.append((regs, comp, offs))
+    # sparse sweeps: positions outside the support are neither loaded nor
+    # read back in the first stage (zeros in registers); without a stage the
+    # tile is stored straight from shared memory and needs the zero fill
+    skip_dead = bool(ld_zero) and bool(stage_info)
+    zk = {k for k in range(K) if (ld_zero >> tin[k]) & 1}
+
+    def emit_stage_read(si, offs):
+        regs, comp, _ = stage_info[si]
+        if si != 0 or not skip_dead:
+            for v in range(NR):
+                w(f"    x[{v}] = tile[sb{si} ^ {offs[v]}u];")
+            return
+        tmask = sum(1 << i for i, k in enumerate(comp) if k in zk)
+        if tmask:
+            w(f"    const bool s0_live = (t & {tmask}) == 0;")
+        for v in range(NR):
+            dead = any((v >> q) & 1 and regs[q] in zk for q in range(rb))
+            if dead:
+                w(f"    x[{v}] = make_double2(0.0, 0.0);")
+            elif tmask:
+                w(f"    x[{v}] = s0_live ? tile[sb{si} ^ {offs[v]}u] : make_double2(0.0, 0.0);")
+            else:
+                w(f"    x[{v}] = tile[sb{si} ^ {offs[v]}u];")
+
     w("  double nrm = 0.0;")
     w(f"  long long tile_id = blockIdx.x;")
 
@@ -304,7 +330,10 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                     dev |= 1 << tin[tb + q]
                     s ^= sw[tb + q]
             if dev & ld_zero:  # outside the support: zero, no memory access
-                w(f"      cp_async16_zero({buf} + (lds_t ^ {s}u), state);")
+                if not skip_dead:
+                    w(f"      cp_async16_zero({buf} + (lds_t ^ {s}u), state);")
+            elif ld_zero and skip_dead:
+                w(f"      if (ld_live) cp_async16({buf} + (lds_t ^ {s}u), state + ({base} | ld_t | {dev}ull));")
             elif ld_zero:
                 w(f"      cp_async16_pred({buf} + (lds_t ^ {s}u), state + ({base} | ld_t | {dev}ull), "
                   "ld_live, state);")
@@ -522,8 +551,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                 if zero_init == 1:
                     w("    if (base == 0ull && t == 0) x[0] = make_double2(1.0, 0.0);")
             else:
-                for v in range(NR):
-                    w(f"    x[{v}] = tile[sb{nxt} ^ {offs[v]}u];")
+                emit_stage_read(nxt, offs)
             cur = nxt
             slot(nxt)
             continue
@@ -701,6 +729,26 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
             offs.append(o)
         stage_info.append((regs, comp, offs))
     TILE = 1 << K
+    skip_dead = bool(ld_zero) and bool(stage_info)
+    zk = {k for k in range(K) if (ld_zero >> tin[k]) & 1}
+
+    def emit_stage_read(si, offs):
+        regs, comp, _ = stage_info[si]
+        if si != 0 or not skip_dead:
+            for v in range(NR):
+                w(f"    x[{v}] = tile[sb{si} ^ {offs[v]}u];")
+            return
+        tmask = sum(1 << i for i, k in enumerate(comp) if k in zk)
+        if tmask:
+            w(f"    const bool s0_live = (t & {tmask}) == 0;")
+        for v in range(NR):
+            dead = any((v >> q) & 1 and regs[q] in zk for q in range(rb))
+            if dead:
+                w(f"    x[{v}] = make_double2(0.0, 0.0);")
+            elif tmask:
+                w(f"    x[{v}] = s0_live ? tile[sb{si} ^ {offs[v]}u] : make_double2(0.0, 0.0);")
+            else:
+                w(f"    x[{v}] = tile[sb{si} ^ {offs[v]}u];")
 
     def prefetch_items(buf, base):
         for it in range(NR):
@@ -710,8 +758,11 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
                 if (it >> q) & 1:
                     dev |= 1 << tin[tb + q]
                     s_ ^= sw[tb + q]
-            if dev & ld_zero:
-                w(f"      cp_async16_zero({buf} + (lds_t ^ {s_}u), state);")
+            if dev & ld_zero:  # outside the support: zero, no memory access
+                if not skip_dead:
+                    w(f"      cp_async16_zero({buf} + (lds_t ^ {s_}u), state);")
+            elif ld_zero and skip_dead:
+                w(f"      if (ld_live) cp_async16({buf} + (lds_t ^ {s_}u), state + ({base} | ld_t | {dev}ull));")
             elif ld_zero:
                 w(f"      cp_async16_pred({buf} + (lds_t ^ {s_}u), state + ({base} | ld_t | {dev}ull), "
                   "ld_live, state);")
@@ -796,8 +847,7 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
                 if zero_init == 1:
                     w("    if (base == 0ull && t == 0) x[0] = make_double2(1.0, 0.0);")
             else:
-                for v in range(NR):
-                    w(f"    x[{v}] = tile[sb{nxt} ^ {offs[v]}u];")
+                emit_stage_read(nxt, offs)
             if nxt == mid:
                 w(f"    if (offset_pending) {{ bar_group(3u, {2 * NT}u); offset_pending = false; }}")
             cur = nxt

@@ -58,3 +58,28 @@ def test_dist_parity_colocated(world):
     assert r.returncode == 0, tail
     assert "0 mismatches" in r.stdout, tail
     print(r.stdout[-2000:])
+
+
+@pytest.mark.gpu
+def test_run_plan_on_a_non_current_device():
+    """run_plan(device='cuda:1') while cuda:0 is current: events, side
+    streams and the JIT launch attributes bind to cuda:1."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import numpy as np
+
+    from paper_2509_14098_b200 import gather, plan as planmod, run_plan
+
+    torch.cuda.set_device(0)
+    plan = planmod.load(str(ROOT / "plans" / "qv20_h18-12.json.gz"))
+    a = run_plan(plan, device="cuda:1")
+    assert a.state.blocks.device == torch.device("cuda", 1)
+    assert torch.cuda.current_device() == 0
+    b = run_plan(plan, device="cuda:0")
+    ga, gb = gather(a.state), gather(b.state)
+    assert np.array_equal(ga, gb)
+    host = torch.from_numpy(ga.reshape(1 << plan.g, -1)).pin_memory()
+    out = torch.empty_like(host).pin_memory()
+    r = run_plan(plan, initial=host, out=out, device="cuda:1", wait=False)
+    r.wait()
+    assert np.array_equal(out.numpy(), r.state.blocks.cpu().numpy())

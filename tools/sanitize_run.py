@@ -38,6 +38,13 @@ for name in ("qft20_h18-12", "qv20_h18-12"):
     _ = compare(gather(b.state), dense)
     _ = sample(dense, 100, 3)
     _ = scatter(dense, plan, 0)
+    from paper_2509_14098_b200 import executor
+
+    _ = executor._gather_chunked(a.state, None)  # chunked host gather (svb_gather_bits)
     n += 2
+# QV-20 from |0...0>: sparse support-only sweeps, two tile groups, sampling CDF walk
+plan = planmod.load(str(ROOT / "plans" / "qv20_h18-12.json.gz"))
+_ = run_plan(plan, shots=500, seed=5)
+n += 1
 torch.cuda.synchronize()
 print(f"sanitize_run: {n} runs ok", flush=True)
