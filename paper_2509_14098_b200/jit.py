@@ -58,29 +58,29 @@ def _lit_raw(x: float) -> str:
 # two UMOVs each (ncu round 2: 1,395 UMOVs beside 3,184 DFMAs per tile of the
 # heaviest QV sweep).  Measured on B200: the table's uniform-register loads
 # raise register pressure into spills and QV-30 ran 667 -> 731 ms, so it is off
-_POOL: dict | None = None
+_CONST_TABLE: dict | None = None
 CONST_POOL = os.environ.get("SVB200_JIT_CONST_POOL", "0") not in ("0", "false", "no")
 _INLINE = {0.0, 1.0, -1.0, 0.5, -0.5, 2.0, -2.0}
 
 
 def _lit(x: float) -> str:
     x = float(x)
-    if _POOL is None or x in _INLINE or x != x:
+    if _CONST_TABLE is None or x in _INLINE or x != x:
         return _lit_raw(x)
     key = x.hex()
-    i = _POOL.setdefault(key, (len(_POOL), x))[0]
+    i = _CONST_TABLE.setdefault(key, (len(_CONST_TABLE), x))[0]
     return f"kc[{i}]"
 
 
 def _pool_begin() -> None:
-    global _POOL
-    _POOL = {} if CONST_POOL else None
+    global _CONST_TABLE
+    _CONST_TABLE = {} if CONST_POOL else None
 
 
 def _pool_end(lines: list) -> list:
     """Insert the constant table after the include line."""
-    global _POOL
-    pool, _POOL = _POOL, None
+    global _CONST_TABLE
+    pool, _CONST_TABLE = _CONST_TABLE, None
     if not pool:
         return lines
     vals = [v for _, v in sorted(pool.values())]
@@ -1213,20 +1213,20 @@ class KernelSlot:
             time.sleep(0.001)
 
 
-_POOL = None
+_COMPILE_POOL = None
 
 
 def compile_async(srcs: list, names: list, threads: int | None = None) -> list:
     """Submit the kernels to the compile pool in launch order (identical
     sources once); the processes of one node start at different offsets and
     share results through the disk cache."""
-    global _POOL
+    global _COMPILE_POOL
     local = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
     lrank = int(os.environ.get("LOCAL_RANK", "0"))
-    if _POOL is None:
+    if _COMPILE_POOL is None:
         # the processes of one node compile at the same time: share the host cores
         n = threads or max(1, min(32, (os.cpu_count() or 4) // max(local, 1)))
-        _POOL = ThreadPoolExecutor(max_workers=n, thread_name_prefix="svb-nvrtc")
+        _COMPILE_POOL = ThreadPoolExecutor(max_workers=n, thread_name_prefix="svb-nvrtc")
     keys = [_key(src) for src in srcs]
     first = {}
     for i, h in enumerate(keys):
@@ -1237,7 +1237,7 @@ def compile_async(srcs: list, names: list, threads: int | None = None) -> list:
         order = order[:1] + order[r:] + order[1:r] if r > 1 else order
     futs = {}
     for i in order:
-        futs[keys[i]] = _POOL.submit(_compile, srcs[i], names[i])
+        futs[keys[i]] = _COMPILE_POOL.submit(_compile, srcs[i], names[i])
     return [KernelSlot(names[i], keys[i], futs[keys[i]]) for i in range(len(srcs))]
 
 
