@@ -155,6 +155,10 @@ SPARSE_START = os.environ.get("SVB200_SPARSE_START", "1") not in ("0", "false", 
 PIPELINED_JIT = os.environ.get("SVB200_JIT_PIPELINE", "1") not in ("0", "false", "no")
 # per-launch CUDA events around every sweep (bench.py's roofline); off by default
 PROFILE_SWEEPS = False
+# self-check mode (SVB200_GUARD_AMPS=n): guard bands of n amplitudes around the
+# state, verified when the run finishes (tests/test_selfcheck_gpu.py)
+GUARD_AMPS = int(os.environ.get("SVB200_GUARD_AMPS", "0"))
+GUARD_VALUE = complex(float("nan"), -7.25)
 _prof_log: list | None = None  # (descriptor, bytes, start event, end event) of the current run
 JIT_MIN_D = int(os.environ.get("SVB200_JIT_MIN_D", "16"))
 # register slots per thread in generated kernels.  4 (256 threads x 16
@@ -447,10 +451,30 @@ class _State:
                 self.buf = torch.empty(max(n, prog.NREG), dtype=torch.complex128, device=device)
             self.buf.record_stream(torch.cuda.current_stream(device))
             self.upload_stream = upload_stream
+        elif GUARD_AMPS:
+            # self-check mode: the state sits between two guard bands filled
+            # with a NaN pattern that run_plan verifies at the end of the run
+            m = max(n, prog.NREG)
+            self.guarded = torch.empty(m + 2 * GUARD_AMPS, dtype=torch.complex128, device=device)
+            self.guarded[:GUARD_AMPS].fill_(GUARD_VALUE)
+            self.guarded[GUARD_AMPS + m:].fill_(GUARD_VALUE)
+            self.buf = self.guarded[GUARD_AMPS:GUARD_AMPS + m]
+            if zero:
+                self.buf.zero_()
         else:
             alloc = torch.zeros if zero else torch.empty
             self.buf = alloc(max(n, prog.NREG), dtype=torch.complex128, device=device)
         self.blocks = self.buf[:n].view(rows, 1 << L)
+
+    def check_guards(self) -> None:
+        g = getattr(self, "guarded", None)
+        if g is None:
+            return
+        bands = torch.cat([g[:GUARD_AMPS], g[-GUARD_AMPS:]])
+        ok = torch.view_as_real(bands).view(torch.int64) == torch.view_as_real(
+            torch.full_like(bands, GUARD_VALUE)).view(torch.int64)
+        if not bool(ok.all()):
+            raise _native.NativeError("guard band around the state was overwritten (out-of-bounds write)")
 
 
 def _upload_stream(device):
@@ -736,6 +760,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
     def finish():
         """Host side of the end of the run: event timings and the drift check."""
         fin_ev.synchronize()
+        state.check_guards()
         if _TRACE and _marks:
             t0 = _marks[0][1]
             stats.trace = [(lab, t0.elapsed_time(ev)) for lab, ev in _marks]

@@ -219,6 +219,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     w = L.append
     _pool_begin()
     w('#include "sweep_jit.cuh"')
+    _emit_check(w, D)
     w(f"// prefetch={os.environ.get('SVB200_JIT_PREFETCH', 'early')}")
     # sweeps that run beside an overlapped remap leave each SM sub-partition
     # room for the remap's one-warp CTA (48 registers): 2 sweep warps per
@@ -333,12 +334,12 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                 if not skip_dead:
                     w(f"      cp_async16_zero({buf} + (lds_t ^ {s}u), state);")
             elif ld_zero and skip_dead:
-                w(f"      if (ld_live) cp_async16({buf} + (lds_t ^ {s}u), state + ({base} | ld_t | {dev}ull));")
+                w(f"      if (ld_live) cp_async16({buf} + (lds_t ^ {s}u), state + chk({base} | ld_t | {dev}ull));")
             elif ld_zero:
-                w(f"      cp_async16_pred({buf} + (lds_t ^ {s}u), state + ({base} | ld_t | {dev}ull), "
+                w(f"      cp_async16_pred({buf} + (lds_t ^ {s}u), state + chk({base} | ld_t | {dev}ull), "
                   "ld_live, state);")
             else:
-                w(f"      cp_async16({buf} + (lds_t ^ {s}u), state + ({base} | ld_t | {dev}ull));")
+                w(f"      cp_async16({buf} + (lds_t ^ {s}u), state + chk({base} | ld_t | {dev}ull));")
         if commit and items:
             w("      cp_async_commit();")
 
@@ -353,7 +354,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
             w("      {")
             w(f"        const double2 v = {buf}[sts_t ^ {s}u];")
             w("        nrm = fma(v.x, v.x, fma(v.y, v.y, nrm));")
-            w(f"        st_stream(state + ({base} | ((st_t | {dev}ull) ^ {st_flip}ull)), v);")
+            w(f"        st_stream(state + chk({base} | ((st_t | {dev}ull) ^ {st_flip}ull)), v);")
             w("      }")
 
     def slot(j):
@@ -588,7 +589,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
         w("  {")
         w(f"    const long long gs = (long long)gridDim.x * {NT};")
         w(f"    for (long long c = (long long)blockIdx.x * {NT} + t; c < {n}ll; c += gs)")
-        w(f"      st_stream(state + (({_deposit('c', free)}){one}), make_double2(0.0, 0.0));")
+        w(f"      st_stream(state + chk(({_deposit('c', free)}){one}), make_double2(0.0, 0.0));")
         w("  }")
     w("  if (norm_out != nullptr) {")
     full = "0xffffffffu" if NT >= 32 else f"{(1 << NT) - 1}u"
@@ -688,6 +689,7 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
     w = L.append
     _pool_begin()
     w('#include "sweep_jit.cuh"')
+    _emit_check(w, D)
     w("// two tile groups")
     w(f'extern "C" __global__ void __launch_bounds__({2 * NT}, 1)')
     w(f"{name}(double2* __restrict__ state, const double2* __restrict__ tab, "
@@ -762,12 +764,12 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
                 if not skip_dead:
                     w(f"      cp_async16_zero({buf} + (lds_t ^ {s_}u), state);")
             elif ld_zero and skip_dead:
-                w(f"      if (ld_live) cp_async16({buf} + (lds_t ^ {s_}u), state + ({base} | ld_t | {dev}ull));")
+                w(f"      if (ld_live) cp_async16({buf} + (lds_t ^ {s_}u), state + chk({base} | ld_t | {dev}ull));")
             elif ld_zero:
-                w(f"      cp_async16_pred({buf} + (lds_t ^ {s_}u), state + ({base} | ld_t | {dev}ull), "
+                w(f"      cp_async16_pred({buf} + (lds_t ^ {s_}u), state + chk({base} | ld_t | {dev}ull), "
                   "ld_live, state);")
             else:
-                w(f"      cp_async16({buf} + (lds_t ^ {s_}u), state + ({base} | ld_t | {dev}ull));")
+                w(f"      cp_async16({buf} + (lds_t ^ {s_}u), state + chk({base} | ld_t | {dev}ull));")
 
     w("  if (threadIdx.x == 0) {")
     w("    for (int b = 0; b < 3; ++b) mbar_init(&mbar[b], " + str(NT) + "u);")
@@ -870,7 +872,7 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
         w("    {")
         w(f"      const double2 v = tile[sts_t ^ {s_}u];")
         w("      nrm = fma(v.x, v.x, fma(v.y, v.y, nrm));")
-        w(f"      st_stream(state + (base | ((st_t | {dev}ull) ^ {st_flip}ull)), v);")
+        w(f"      st_stream(state + chk(base | ((st_t | {dev}ull) ^ {st_flip}ull)), v);")
         w("    }")
     if not zero_init:
         w(f"    bar_group(bar_id, {NT}u);")
@@ -892,7 +894,7 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
         w("  {")
         w(f"    const long long gs = (long long)gridDim.x * {2 * NT};")
         w(f"    for (long long c = (long long)blockIdx.x * {2 * NT} + threadIdx.x; c < {n}ll; c += gs)")
-        w(f"      st_stream(state + (({_deposit('c', free)}){one}), make_double2(0.0, 0.0));")
+        w(f"      st_stream(state + chk(({_deposit('c', free)}){one}), make_double2(0.0, 0.0));")
         w("  }")
     w("  if (norm_out != nullptr) {")
     for o in (16, 8, 4, 2, 1):
@@ -907,6 +909,19 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
     w("  }")
     w("}")
     return "\n".join(_pool_end(L)) + "\n"
+
+
+# SVB200_JIT_CHECK=1: every global state index of a generated kernel is
+# bounds-checked (trap) against the device's 2^D amplitudes -- the self-check
+# mode that replaces compute-sanitizer on pools where it is unavailable
+CHECK = os.environ.get("SVB200_JIT_CHECK", "0") not in ("0", "false", "no")
+
+
+def _emit_check(w, D: int) -> None:
+    if CHECK:
+        w(f"SVB_F u64 chk(u64 i) {{ if (i >= {1 << D}ull) __trap(); return i; }}")
+    else:
+        w("#define chk(i) (i)")
 
 
 def _phase_base(w, op, coef_c0: complex, K: int, rb: int) -> None:
