@@ -292,6 +292,12 @@ int svb_cdf_walk(const double* q, int64_t n, const double* cstart, const double*
 int svb_cdf_search(const double* q, int64_t n, const double* cend_all, int64_t nchunks_all, int64_t my_lo,
                    int64_t my_hi, double c_last, const double* u, int64_t nshots, int64_t index_base,
                    int64_t* out, void* stream);
+/* svb_region_move: in place, region dst_sel of the m local bits lbits
+ *   (selector bit m-1-i <-> lbits[i], like svb_pack_region) takes the
+ *   amplitudes of region src_sel: the remap after a replicated sparse prefix
+ *   (program.localize_applies), which moves no data between GPUs. */
+int svb_region_move(svb_c128* state, int nbits, const int32_t* lbits, int m, uint32_t src_sel, uint32_t dst_sel,
+                    void* stream);
 /* svb_gather_bits: dst[t] = src[P(base + t)], t < count, with
  *   P(f) = sum_k bit_k(f) << perm[k] (one chunk of a permuted order: the
  *   chunked gather of a sharded state, svpart/executor.py:310-326). */

@@ -61,6 +61,7 @@ _SIGS = {
     "svb_stream_wait_u32": ([_vp, _u32, _vp], _int),
     "svb_stream_create": ([_c.POINTER(_vp)], _int),
     "svb_gather_bits": ([_vp, _int, _pi32, _c.c_uint64, _i64, _vp, _vp], _int),
+    "svb_region_move": ([_vp, _int, _pi32, _int, _u32, _u32, _vp], _int),
     "svb_cdf_chunk_elems": ([], _i64),
     "svb_probs_numpy": ([_vp, _int, _pi32, _vp, _vp], _int),
     "svb_deposit_scatter": ([_vp, _i64, _int, _pi32, _c.c_uint64, _vp, _vp], _int),

@@ -307,6 +307,20 @@ __global__ void k_gather_bits(const double2* __restrict__ src, double2* __restri
   }
 }
 
+// state[region dst][k] = state[region src][k]: one region of the swapped
+// local bits moved onto another (the local remap after a replicated prefix)
+__global__ void k_region_move(double2* __restrict__ s, const __grid_constant__ Region r, uint64_t dst_mask,
+                              uint64_t count) {
+  __shared__ uint64_t lut[5 * 256];
+  for (int i = threadIdx.x; i < r.nchunks * 256; i += blockDim.x) lut[i] = r.lut[i];
+  __syncthreads();
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < count; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = region_index(lut, r.nchunks, r.L, r.m, r.selmask, k);
+    const uint64_t b = (a & ~r.selmask) | dst_mask;
+    st_stream(s + b, ld_stream(s + a));
+  }
+}
+
 int grid_for(uint64_t work, int threads) {
   uint64_t b = (work + threads - 1) / threads;
   const uint64_t cap = (uint64_t)num_sms() * 32;
@@ -499,5 +513,20 @@ extern "C" int svb_gather_bits(const svb_c128* src, int nbits, const int32_t* pe
   k_gather_bits<<<grid_for((uint64_t)count, 256), 256, 0, as_stream(stream)>>>(
       reinterpret_cast<const double2*>(src), reinterpret_cast<double2*>(dst), nbits, lut, base, (uint64_t)count);
   SVB_CHECK_LAUNCH("svb_gather_bits");
+  return SVB_OK;
+}
+
+extern "C" int svb_region_move(svb_c128* state, int nbits, const int32_t* lbits, int m, uint32_t src_sel,
+                               uint32_t dst_sel, void* stream) {
+  Region r;
+  if (int rc = make_region(1, nbits, lbits, m, src_sel, r)) return rc;
+  if (src_sel == dst_sel) return SVB_OK;
+  uint64_t dst_mask = 0;
+  for (int i = 0; i < m; ++i)
+    if ((dst_sel >> (m - 1 - i)) & 1) dst_mask |= uint64_t(1) << lbits[i];
+  const uint64_t count = uint64_t(1) << (nbits - m);
+  k_region_move<<<grid_for(count, 256), 256, 0, as_stream(stream)>>>(reinterpret_cast<double2*>(state), r, dst_mask,
+                                                                      count);
+  SVB_CHECK_LAUNCH("svb_region_move");
   return SVB_OK;
 }

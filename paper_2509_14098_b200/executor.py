@@ -151,6 +151,9 @@ def _dist_info(group=None):
 # runs from |0...0> compute only the support of the state until it covers
 # the device (program.sparse_start)
 SPARSE_START = os.environ.get("SVB200_SPARSE_START", "1") not in ("0", "false", "no")
+# runs from |0...0> whose first remap follows only sparse sweeps: every process
+# computes that prefix itself and the remap moves no data (program.localize_applies)
+LOCALIZE = os.environ.get("SVB200_LOCALIZE", "1") not in ("0", "false", "no")
 # generated kernels compile in the background; each launch waits only for its own
 PIPELINED_JIT = os.environ.get("SVB200_JIT_PIPELINE", "1") not in ("0", "false", "no")
 # per-launch CUDA events around every sweep (bench.py's roofline); off by default
@@ -220,14 +223,16 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
     t0 = time.perf_counter()
     dist_run = _dist_info()[1] > 1
     ob = _overlap_bits() if (use_jit and dist_run) else 0
-    skip_first = False
-    if ob and zero_start and SPARSE_START:
+    skip_first = replicate = False
+    world = _dist_info()[1]
+    if use_jit and zero_start and SPARSE_START and world > 1:
         dp0 = prog.plan_device(plan, geo, rb=JIT_REG_BITS, overlap_bits=0, free_start=True,
                                stable_threads=jitmod_shuffle())
         skip_first = prog.sparse_reaches_first_remap(dp0, geo.D)
+        replicate = LOCALIZE and prog.localize_applies(dp0, geo.D, world, geo.h)
     dp = prog.plan_device(plan, geo, rb=JIT_REG_BITS if use_jit else prog.RB, overlap_bits=ob,
                           free_start=zero_start, stable_threads=use_jit and jitmod_shuffle(),
-                          overlap_skip_first=skip_first)
+                          overlap_skip_first=skip_first, replicate_prefix=replicate)
     blob, descs, _ = prog.pack(dp.buf)
     host = np.ascontiguousarray(blob)
     dev_blob = torch.from_numpy(host).to(device)
@@ -252,7 +257,8 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
         from . import jit as jitmod
 
         t1 = time.perf_counter()
-        sparse = prog.sparse_start(dp, geo.D, geo.rank_base == 0) if (zero_start and SPARSE_START) else {}
+        unit = geo.rank_base == 0 or any(st.kind == "localize" for st in dp.steps)  # replicas hold it too
+        sparse = prog.sparse_start(dp, geo.D, unit) if (zero_start and SPARSE_START) else {}
         names, slots = jitmod.build_kernels(dp.buf, sparse=sparse, lazy=PIPELINED_JIT)
         out.zero_init = dict(jitmod._LAST_ZERO_INIT)
         out.sparse = sparse
@@ -677,7 +683,9 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             swaps = task.payload["swaps"]
             m = len(swaps)
             xst = compiled.steps[task.id]
-            if compiled.overlap.get(xst.pre, {}).get("pre") is xst:
+            if xst.kind == "localize":
+                launches = _localize(state, xst, geo, stream)
+            elif compiled.overlap.get(xst.pre, {}).get("pre") is xst:
                 launches, ce0, ce1 = _remap_overlapped(state, xst, geo, group, ovl)
                 events.append(("Exchange", ce0, ce1))
             else:
@@ -688,7 +696,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             moved = nranks * ((1 << m) - 1) * (1 << (L - m))
             messages = nranks * ((1 << m) - 1)
             mr = sum(1 for ib, _ in xst.swaps if ib >= geo.h)  # swapped bits that cross GPUs
-            if mr:  # this process's bytes over NVLink (sent = received)
+            if mr and xst.kind != "localize":  # this process's bytes over NVLink (sent = received)
                 stats.nvlink_bytes += 16 * rows * ((1 << mr) - 1) * (1 << (L - mr))
             packed["sent"] = True
             stats.amps_moved += moved
@@ -1029,6 +1037,30 @@ def _run_descs(compiled, first, count, state, rows_eff, L, norms, grid_limit, st
         _prof_end(ev, first + i, compiled.desc_bytes[first + i])
         launches += 1
     return launches
+
+
+def _localize(state: _State, st, geo: prog.DeviceGeometry, stream) -> int:
+    """The remap after a replicated sparse prefix (program.localize_applies):
+    this process holds the prefix state of the process with the unit
+    amplitude, and after the reference's Pack/Exchange/Unpack it would hold
+    that state's region alpha (its own id bits at the swapped rank bits,
+    executor.py:235-243) at region 0 of the swapped local bits, zeros
+    elsewhere.  Region alpha moves to region 0 in HBM; the other regions are
+    left stale and read as zeros by the next (sparse) sweep."""
+    lib = _native.load()
+    me = geo.rank_base >> geo.h
+    alpha = 0
+    lbits = []
+    for ib, lb in st.swaps:
+        alpha = (alpha << 1) | ((me >> (ib - geo.h)) & 1)
+        lbits.append(lb)
+    if alpha == 0:
+        return 0
+    flat = _Flat(state)
+    arr, l32 = _native.i32_array(lbits)
+    _native.check(lib.svb_region_move(state.buf.data_ptr(), flat.L, l32, len(lbits), alpha, 0, stream),
+                  "svb_region_move")
+    return 1
 
 
 def _remap(state: _State, swaps: list, geo: prog.DeviceGeometry, group, stream) -> int:

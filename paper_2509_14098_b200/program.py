@@ -708,7 +708,7 @@ def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int, max_chain: 
         # sweeps on each side, nearest first; relabel-only leaves move no data
         before = []
         for x in reversed(steps[:i]):
-            if x.kind == "exchange":
+            if x.kind in ("exchange", "localize"):  # a replicated sparse prefix stays whole
                 break
             before.extend(range(x.first + x.count - 1, x.first - 1, -1))
         nxt = None
@@ -753,7 +753,7 @@ def _plan_overlap(steps: list, buf, geo: DeviceGeometry, nbits: int, max_chain: 
 def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_BITS,
                 max_materialize: int = 64, rb: int = RB, fuse: bool = True,
                 overlap_bits: int = 0, free_start: bool = True, stable_threads: bool = False,
-                overlap_skip_first: bool = False) -> DeviceProgram:
+                overlap_skip_first: bool = False, replicate_prefix: bool = False) -> DeviceProgram:
     """Compile every ApplyFused task of a plan for one device, with a global layout.
 
     The physical layout is a permutation `where` of the local bits that the
@@ -771,13 +771,27 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
     L, D = geo.L, geo.D
     K = min(kmax, D)
     low = min(low, K)
+    # replicate_prefix (run from |0...0>, see localize_applies): every
+    # process computes the sweeps before the first remap as the process that
+    # holds the unit amplitude, and that remap becomes a local region move
+    first_remote = None
+    if replicate_prefix:
+        for ti, task in enumerate(plan.tasks):
+            if task.kind == "Exchange" and any(geo.g - 1 - sw["rank_bit"] >= geo.h for sw in task.payload["swaps"]):
+                first_remote = ti
+                break
+    geo0 = DeviceGeometry(d=geo.d, g=geo.g, h=geo.h, rank_base=0, pad_to=geo.pad_to)
+    prefix_ids = set()
     raw = {}
-    for task in plan.tasks:
+    for ti, task in enumerate(plan.tasks):
         if task.kind == "ApplyFused":
             layout = plan.layout_phases[task.payload["phase"]]
+            in_prefix = first_remote is not None and ti < first_remote
+            if in_prefix:
+                prefix_ids.add(task.id)
             prims = []
             for e in task.payload["gates"]:
-                prims.extend(resolve_entry(e, layout, geo))
+                prims.extend(resolve_entry(e, layout, geo0 if in_prefix else geo))
             raw[task.id] = prims
     # segments: runs of ApplyFused tasks with no remap between them.  With
     # MERGE_LEAVES the gate fusion runs over a whole segment (an SU(4) split
@@ -937,6 +951,8 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
                 done.append(task_slot[seg[completed].id])
                 completed += 1
             sp.norm_slot = done[-1] if done else -1
+            if seg[0].id in prefix_ids and geo.rank_base != 0:
+                sp.norm_slot = -1  # a replica of process 0's prefix: its norm counts once
             for sl in done:
                 norm_alias[sl] = done[-1]
             if done:
@@ -970,7 +986,10 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
                 where[L + ib], where[lb] = where[lb], where[L + ib]
             else:
                 sw.append((ib, where[lb]))
-        steps.append(Step("exchange", task.id, swaps=sw))
+        # the first remote remap after a replicated prefix moves no data
+        # between GPUs (localize_applies): each process keeps its region
+        kind = "localize" if (first_remote is not None and plan.tasks.index(task) == first_remote) else "exchange"
+        steps.append(Step(kind, task.id, swaps=sw))
     if seg:
         run_segment(seg)
     slot = len(task_slot)
@@ -1035,6 +1054,12 @@ def sparse_start(dp: "DeviceProgram", D: int, unit: bool) -> dict:
     for st in dp.steps:
         if stop:
             break
+        if st.kind == "localize":
+            # the region of this process moved to region 0 of the swapped
+            # bits; the other regions hold stale prefix data, read as zeros
+            if supp is not None:
+                supp &= ~sum(1 << lb for _, lb in st.swaps)
+            continue
         if st.kind == "exchange":
             if st.swaps:
                 break
@@ -1057,6 +1082,23 @@ def sparse_start(dp: "DeviceProgram", D: int, unit: bool) -> dict:
     if s0 == 0 and not any(int(o["kind"]) == OP_STAGE for o in ops):
         return {}
     return {i: (s, k == len(seq) - 1) for k, (i, s) in enumerate(seq)}
+
+
+def localize_applies(dp: "DeviceProgram", D: int, world: int, h: int) -> bool:
+    """From |0...0> every sweep before the first inter-process remap is sparse
+    (cheap), and that remap swaps every process-id bit.  Then after the remap
+    process w holds exactly region alpha_w (its id bits) of the state that
+    the process holding the unit amplitude had before it, moved to region 0
+    of the swapped local bits, and zeros elsewhere: every process can compute
+    that prefix itself (a replica, a fraction of a pass) and move its region
+    locally, so no amplitude crosses NVLink for that remap."""
+    if world < 2 or not sparse_reaches_first_remap(dp, D):
+        return False
+    for st in dp.steps:
+        if st.kind == "exchange" and st.swaps:
+            ids = {ib - h for ib, _ in st.swaps if ib >= h}
+            return ids == set(range(world.bit_length() - 1))
+    return False
 
 
 def sparse_reaches_first_remap(dp: "DeviceProgram", D: int) -> bool:

@@ -203,7 +203,7 @@ def _devmap(jt: np.ndarray, tin) -> np.ndarray:
 
 
 def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog.RB, stable: bool = False,
-                 sparse: bool = False, kmax: int = prog.KMAX):
+                 sparse: bool = False, kmax: int = prog.KMAX, localize: bool = False):
     """Run a plan through the compiled device programs of `world` devices.
 
     Each device gets its own program (plan_device with its rank range);
@@ -216,9 +216,14 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
     rows = nr // world
     h = rows.bit_length() - 1
     progs, parts = [], []
+    replicate = False
+    if localize and sparse and world > 1:  # decided on the unit-holding process, as the executor does
+        geo0 = prog.DeviceGeometry(d=d, g=g, h=h, rank_base=0, pad_to=prog.RB)
+        replicate = prog.localize_applies(prog.plan_device(plan, geo0, rb=rb, stable_threads=stable, kmax=kmax),
+                                          geo0.D, world, h)
     for w in range(world):
         geo = prog.DeviceGeometry(d=d, g=g, h=h, rank_base=w * rows, pad_to=prog.RB)
-        dp = prog.plan_device(plan, geo, rb=rb, stable_threads=stable, kmax=kmax)
+        dp = prog.plan_device(plan, geo, rb=rb, stable_threads=stable, kmax=kmax, replicate_prefix=replicate)
         blob, descs, p = prog.pack(dp.buf)
         progs.append((geo, dp, descs, p))
     D = progs[0][0].D
@@ -231,7 +236,7 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
     states[0][0] = 1.0
     sp_of = []  # per device: descriptor -> (support, full_out)
     for w, (geo, dp, descs, p) in enumerate(progs):
-        sp = prog.sparse_start(dp, D, w == 0) if sparse else {}
+        sp = prog.sparse_start(dp, D, w == 0 or replicate) if sparse else {}
         if sp:  # unwritten memory: any read outside the support would poison the result
             states[w][:] = np.nan
         sp_of.append(sp)
@@ -247,6 +252,26 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
                            [sp_of[w].get(i) for i in range(sw.first, sw.first + sw.count)])
             if st.count == 0 and slot not in progs[0][1].norm_alias:
                 norms[slot] = norms[slot - 1] if slot else 1.0  # |0...0> (maybe not materialised yet)
+        elif task.kind == "Exchange" and st.kind == "localize":
+            # every device moves region alpha (its id bits) of its replica to region 0
+            for w in range(world):
+                me = w
+                alpha, lbs = 0, []
+                for ib, lb in st.swaps:
+                    alpha = (alpha << 1) | ((me >> (ib - h)) & 1)
+                    lbs.append(lb)
+                if alpha:
+                    m = len(lbs)
+                    idx = np.arange(1 << D, dtype=np.int64)
+                    sel = np.zeros_like(idx)
+                    for i, lb in enumerate(lbs):
+                        sel |= ((idx >> lb) & 1) << (m - 1 - i)
+                    dst = idx[sel == 0]
+                    src = dst.copy()
+                    for i, lb in enumerate(lbs):
+                        if (alpha >> (m - 1 - i)) & 1:
+                            src |= 1 << lb
+                    states[w][dst] = states[w][src]
         elif task.kind == "Exchange":
             # global index = device * 2^(L+h) + row * 2^L + local
             full = np.concatenate([s[: rows << L] for s in states])

@@ -112,3 +112,25 @@ def test_stable_thread_orders():
     assert set(orders[0][5:]) <= {8, 9, 10, 11}
     assert prog.unpack_order(prog.pack_order(orders[2]), K - 4) == orders[2]
     assert prog._thread_orders(stages, K, stable=False)[1] == [2, 3, 6, 7, 8, 9, 10, 11]
+
+
+
+@pytest.mark.parametrize("world,kmax", [(2, 12), (4, 12), (2, 6), (4, 7), (8, 12)])
+def test_localized_first_remap_matches_reference(grid_docs, grid_states, world, kmax):
+    """Runs from |0...0> whose first remap follows only sparse sweeps: every
+    device computes the prefix as the unit-holding device and the remap is
+    a local region move (program.localize_applies)."""
+    from paper_2509_14098_b200 import program as prog
+
+    n = used = 0
+    for doc in _cases(grid_docs, grid_states, min_ranks=world):
+        plan = plan_from_doc(doc["plan"])
+        blocks, norms = program_emu.emulate_plan(plan, world=world, sparse=True, kmax=kmax, localize=True)
+        err = float(np.max(np.abs(blocks - grid_states[doc["name"]])))
+        assert err < TOL, (doc["name"], world, err)
+        assert np.all(np.abs(norms - 1) < 1e-8), doc["name"]
+        rows = (1 << plan.g) // world
+        geo = prog.DeviceGeometry(d=plan.d, g=plan.g, h=rows.bit_length() - 1, rank_base=0, pad_to=prog.RB)
+        used += prog.localize_applies(prog.plan_device(plan, geo, kmax=kmax), geo.D, world, geo.h)
+        n += 1
+    assert n > 20 and used > 5, (n, used)

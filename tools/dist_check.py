@@ -73,7 +73,9 @@ def scale_checks(me, world):
 
     bad = n = 0
     lg = world.bit_length() - 1
-    names = [(f"qft{30 + lg}_h30-12", 0x2B3C5D1 << lg | 1)]
+    # a basis state (dense sweeps, the NVLink remap) and |0...0> (sparse sweeps;
+    # the first remap is localized: every process replicates the prefix)
+    names = [(f"qft{30 + lg}_h30-12", 0x2B3C5D1 << lg | 1), (f"qft{30 + lg}_h30-12", 0)]
     if "--qft34" in sys.argv:
         names.append((f"qft34_h{34 - lg}-12", 0))
     for name, x in names:
