@@ -516,7 +516,10 @@ def main() -> None:
                                     "bytes_per_step": acc["sweep_bytes"] // args.steps,
                                     "launches_per_step": sweeps // args.steps,
                                     "sweep_ms_per_step": 1e3 * compute_s / args.steps},
-                     "fp64_pipe_pct": fp64},
+                     "fp64_pipe_pct": fp64,
+                     "frac_dram": (traffic / (dom_ms / 1e3) / 1e9 / peak) if traffic else None,
+                     "frac_dram_note": "ncu DRAM bytes (read + write) of this kernel per launch / its event-timed "
+                                       "launch / peak; traffic from profiles/traffic.json (same code revision)"},
         "e2e": e2e,
         "gpu_launches": launches,
         "compile_ms": 1e3 * stats.compile_seconds,

@@ -37,8 +37,11 @@ CTAB_AHEAD = os.environ.get("SVB200_JIT_CTAB_AHEAD", "1") not in ("0", "false", 
 NO_AHEAD_ZERO = os.environ.get("SVB200_JIT_NO_AHEAD_ZERO", "1") not in ("0", "false", "no")
 # stage changes that keep the warp-level thread bits move data with warp shuffles
 SHUFFLE_STAGES = os.environ.get("SVB200_JIT_SHUFFLE", "0") not in ("0", "false", "no")  # measured: slower
-# FP64-heavy sweeps run two tile groups per CTA (kernel_source_2g)
-GROUPS = os.environ.get("SVB200_JIT_GROUPS", "1") not in ("0", "false", "no")
+# FP64-heavy sweeps can run two tile groups per CTA (kernel_source_2g,
+# SVB200_JIT_GROUPS=1).  Off by default: it gained 2-4% on QV-30, and forcing
+# it onto every sweep (SVB200_JIT_GROUPS_MIN_DFMA=0) exposed wrong norms on
+# phase-table QFT sweeps and a stall on a sparse one (round 2, unresolved)
+GROUPS = os.environ.get("SVB200_JIT_GROUPS", "0") not in ("0", "false", "no")
 NVRTC_OPTS = ["--gpu-architecture=sm_100a", "--std=c++17", f"-I{CSRC}", "-lineinfo",
               "--extra-device-vectorization"]
 
@@ -271,7 +274,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     # sparse sweeps: positions outside the support are neither loaded nor
     # read back in the first stage (zeros in registers); without a stage the
     # tile is stored straight from shared memory and needs the zero fill
-    skip_dead = bool(ld_zero) and bool(stage_info)
+    skip_dead = SKIP_DEAD and bool(ld_zero) and bool(stage_info)
     zk = {k for k in range(K) if (ld_zero >> tin[k]) & 1}
 
     def emit_stage_read(si, offs):
@@ -608,6 +611,8 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     return "\n".join(_pool_end(L)) + "\n"
 
 
+GROUP_OFFSET = os.environ.get("SVB200_JIT_GROUP_OFFSET", "1") not in ("0", "false", "no")
+SKIP_DEAD = os.environ.get("SVB200_JIT_SKIP_DEAD", "1") not in ("0", "false", "no")
 # sweeps whose FP64 work per amplitude reaches this many DFMA (a fused 4x4 is
 # 16) run two tile groups per CTA (kernel_source_2g)
 GROUPS_MIN_DFMA = float(os.environ.get("SVB200_JIT_GROUPS_MIN_DFMA", "48"))
@@ -731,7 +736,7 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
             offs.append(o)
         stage_info.append((regs, comp, offs))
     TILE = 1 << K
-    skip_dead = bool(ld_zero) and bool(stage_info)
+    skip_dead = SKIP_DEAD and bool(ld_zero) and bool(stage_info)
     zk = {k for k in range(K) if (ld_zero >> tin[k]) & 1}
 
     def emit_stage_read(si, offs):
@@ -791,7 +796,7 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
     # the middle of its first tile, so one group's stages and stores fall in
     # the other's FP64 phase (started together they stay in lockstep)
     nst = len(stage_info)
-    mid = nst // 2 if nst >= 2 else None
+    mid = nst // 2 if (nst >= 2 and GROUP_OFFSET) else None
     if mid is not None:
         w("  bool offset_pending = grp == 0;")
         w(f"  if (grp == 1) bar_group(3u, {2 * NT}u);")
