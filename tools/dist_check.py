@@ -86,7 +86,8 @@ def scale_checks(me, world):
             comm.release_arenas()
             torch.cuda.empty_cache()
         rows = (1 << plan.g) // world
-        init = basis_blocks(plan, x, me * rows, rows, "cuda") if x else None
+        # processes sharing one GPU keep the initial blocks in host memory
+        init = basis_blocks(plan, x, me * rows, rows, "cpu" if "--colocate" in sys.argv else "cuda") if x else None
         res = run_plan(plan, initial=init)
         del init
         err = qft_closed_form_err(res.state, x)
