@@ -259,7 +259,8 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
         t1 = time.perf_counter()
         unit = geo.rank_base == 0 or any(st.kind == "localize" for st in dp.steps)  # replicas hold it too
         sparse = prog.sparse_start(dp, geo.D, unit) if (zero_start and SPARSE_START) else {}
-        names, slots = jitmod.build_kernels(dp.buf, sparse=sparse, lazy=PIPELINED_JIT)
+        ld_xor = _fold_localize(dp, geo, sparse)
+        names, slots = jitmod.build_kernels(dp.buf, sparse=sparse, lazy=PIPELINED_JIT, ld_xor=ld_xor)
         out.zero_init = dict(jitmod._LAST_ZERO_INIT)
         out.sparse = sparse
         for i, gcount in jitmod._LAST_GROUPS.items():  # launch geometry of two-group kernels
@@ -1039,6 +1040,42 @@ def _run_descs(compiled, first, count, state, rows_eff, L, norms, grid_limit, st
     return launches
 
 
+def _alpha(st, geo: prog.DeviceGeometry) -> int:
+    """This process's id bits at a remap's swapped rank bits (selector order)."""
+    me = geo.rank_base >> geo.h
+    alpha = 0
+    for ib, _ in st.swaps:
+        alpha = (alpha << 1) | ((me >> (ib - geo.h)) & 1)
+    return alpha
+
+
+def _fold_localize(dp, geo: prog.DeviceGeometry, sparse: dict) -> dict:
+    """Localized remaps whose next sweep is sparse and holds every swapped
+    local bit in its tile: that sweep reads region alpha through an XOR of
+    its load addresses (no region move).  Returns {descriptor: xor mask} and
+    marks the steps folded."""
+    out = {}
+    steps = dp.steps
+    for i, st in enumerate(steps):
+        if st.kind != "localize":
+            continue
+        nxt = next((x for x in steps[i + 1:] if x.kind in ("sweeps", "materialize") and x.count), None)
+        if nxt is None or nxt.first not in sparse:
+            continue
+        d = dp.buf.descs[nxt.first]
+        tin = set(int(b) for b in d["tin"][:d["K"]])
+        if not all(lb in tin for _, lb in st.swaps):
+            continue
+        alpha, m, mask = _alpha(st, geo), len(st.swaps), 0
+        for j, (_, lb) in enumerate(st.swaps):
+            if (alpha >> (m - 1 - j)) & 1:
+                mask |= 1 << lb
+        if mask:
+            out[nxt.first] = mask
+        st.folded = True
+    return out
+
+
 def _localize(state: _State, st, geo: prog.DeviceGeometry, stream) -> int:
     """The remap after a replicated sparse prefix (program.localize_applies):
     this process holds the prefix state of the process with the unit
@@ -1048,13 +1085,9 @@ def _localize(state: _State, st, geo: prog.DeviceGeometry, stream) -> int:
     elsewhere.  Region alpha moves to region 0 in HBM; the other regions are
     left stale and read as zeros by the next (sparse) sweep."""
     lib = _native.load()
-    me = geo.rank_base >> geo.h
-    alpha = 0
-    lbits = []
-    for ib, lb in st.swaps:
-        alpha = (alpha << 1) | ((me >> (ib - geo.h)) & 1)
-        lbits.append(lb)
-    if alpha == 0:
+    alpha = _alpha(st, geo)
+    lbits = [lb for _, lb in st.swaps]
+    if alpha == 0 or getattr(st, "folded", False):  # folded: the next sweep reads region alpha
         return 0
     flat = _Flat(state)
     arr, l32 = _native.i32_array(lbits)

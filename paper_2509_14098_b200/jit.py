@@ -163,8 +163,12 @@ def _warp_local_change(stage_info: list, a: int, b: int, nthreads: int) -> bool:
 
 
 def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int = 0,
-                  sparse: tuple | None = None) -> str:
+                  sparse: tuple | None = None, ld_xor: int = 0) -> str:
     """Straight-line kernel for one sweep.
+
+    ld_xor: tile bits XOR-ed into every load address (the first sweep after a
+    localized remap reads region alpha of the swapped bits as region 0; the
+    bits are tile bits, so every tile still reads only its own positions).
 
     zero_init: 0 = load the state; 1 = the input is |0...0> with the unit
     amplitude on this device (synthesise tiles, no loads); 2 = the input is
@@ -198,6 +202,8 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     fpos = {b: i for i, b in enumerate(fbits)}
     tb = K - rb  # thread bits
     tinmask = sum(1 << b for b in tin)
+    assert not ld_xor & ~tinmask, "load XOR must stay within the tile"
+    xr = f" ^ {ld_xor}ull" if ld_xor else ""
     ld_zero = 0  # tile bits whose loaded amplitudes are known zero (zero-filled)
     NTV = "ntiles"  # tiles this launch enumerates
     dead_slabs = []  # (fixed bit set to 1, free bits) covering the dead positions
@@ -337,12 +343,12 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                 if not skip_dead:
                     w(f"      cp_async16_zero({buf} + (lds_t ^ {s}u), state);")
             elif ld_zero and skip_dead:
-                w(f"      if (ld_live) cp_async16({buf} + (lds_t ^ {s}u), state + chk({base} | ld_t | {dev}ull));")
+                w(f"      if (ld_live) cp_async16({buf} + (lds_t ^ {s}u), state + chk(({base} | ld_t | {dev}ull){xr}));")
             elif ld_zero:
-                w(f"      cp_async16_pred({buf} + (lds_t ^ {s}u), state + chk({base} | ld_t | {dev}ull), "
+                w(f"      cp_async16_pred({buf} + (lds_t ^ {s}u), state + chk(({base} | ld_t | {dev}ull){xr}), "
                   "ld_live, state);")
             else:
-                w(f"      cp_async16({buf} + (lds_t ^ {s}u), state + chk({base} | ld_t | {dev}ull));")
+                w(f"      cp_async16({buf} + (lds_t ^ {s}u), state + chk(({base} | ld_t | {dev}ull){xr}));")
         if commit and items:
             w("      cp_async_commit();")
 
@@ -1170,7 +1176,8 @@ def _nvrtc(src: str, name: str, h: str) -> bytes:
 
 
 def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: int | None = None,
-                  zero_init: dict | None = None, sparse: dict | None = None, lazy: bool = False):
+                  zero_init: dict | None = None, sparse: dict | None = None, lazy: bool = False,
+                  ld_xor: dict | None = None):
     """Generate + compile one kernel per sweep descriptor; returns (names, cubins).
 
     zero_init maps descriptor index -> 1/2 for sweeps whose input is known to
@@ -1198,7 +1205,12 @@ def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: in
         gen = kernel_source_2g if two else kernel_source
         if two:
             groups[i] = 2
-        body = gen("KNAME", d, ops, buf.coef, zi, sparse.get(i))
+        if (ld_xor or {}).get(i):
+            gen = kernel_source  # the one-group kernel carries the load XOR
+            groups.pop(i, None)
+            body = gen("KNAME", d, ops, buf.coef, zi, sparse.get(i), ld_xor[i])
+        else:
+            body = gen("KNAME", d, ops, buf.coef, zi, sparse.get(i))
         h = hashlib.sha1(body.encode()).hexdigest()[:16]
         name = f"{prefix}_{h}"
         srcs.append(body.replace("KNAME", name))

@@ -579,6 +579,8 @@ class Step:
     # sweeps before the remap that run depth-first in parts (oldest first,
     # ending with `pre`): chunk c of all of them, then chunk c of the remap
     chain: list = field(default_factory=list)
+    # localize: the next sweep reads region alpha through a load XOR (no region move)
+    folded: bool = False
 
 
 @dataclass

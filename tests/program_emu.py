@@ -30,7 +30,8 @@ def _xor_img(vals: np.ndarray, imgs) -> np.ndarray:
     return out
 
 
-def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None, sparse=None) -> None:
+def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None, sparse=None,
+               ld_xor=None) -> None:
     """In-place on the flat device state (length 2^D).
 
     sparse: per descriptor (support, full_out) or None (program.sparse_start);
@@ -41,6 +42,7 @@ def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None,
     cofs_base = 0
     for di, d in enumerate(descs):
         sp = sparse[di] if sparse is not None else None
+        lx = (ld_xor[di] or 0) if ld_xor is not None else 0
         K, D = int(d["K"]), int(d["D"])
         RB = int(d["rb"])
         NR = 1 << RB
@@ -84,9 +86,9 @@ def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None,
                 tile[ld_s] = state[base | ld_dev]
             elif sp[0] == 0:  # synthesised |0...0>
                 tile[ld_s] = np.where((base | ld_dev) == 0, 1.0 + 0j, 0j)
-            else:  # zero-filled outside the support
+            else:  # zero-filled outside the support (a folded localize reads region alpha)
                 pos = base | ld_dev
-                tile[ld_s] = np.where((pos & ~sp[0]) == 0, state[pos], 0j)
+                tile[ld_s] = np.where((pos & ~sp[0]) == 0, state[pos ^ lx], 0j)
             x = None
             J = None
             dev_base = None
@@ -203,7 +205,7 @@ def _devmap(jt: np.ndarray, tin) -> np.ndarray:
 
 
 def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog.RB, stable: bool = False,
-                 sparse: bool = False, kmax: int = prog.KMAX, localize: bool = False):
+                 sparse: bool = False, kmax: int = prog.KMAX, localize: bool = False, fold: bool = True):
     """Run a plan through the compiled device programs of `world` devices.
 
     Each device gets its own program (plan_device with its rank range);
@@ -234,9 +236,15 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
                 [(s.kind, s.task_id, s.swaps) for s in progs[0][1].steps]
     states = [np.zeros(1 << D, dtype=np.complex128) for _ in range(world)]
     states[0][0] = 1.0
-    sp_of = []  # per device: descriptor -> (support, full_out)
+    sp_of, lx_of = [], []  # per device: descriptor -> (support, full_out); descriptor -> load XOR
     for w, (geo, dp, descs, p) in enumerate(progs):
         sp = prog.sparse_start(dp, D, w == 0 or replicate) if sparse else {}
+        if replicate and fold:
+            from paper_2509_14098_b200.executor import _fold_localize
+
+            lx_of.append(_fold_localize(dp, geo, sp))
+        else:
+            lx_of.append({})
         if sp:  # unwritten memory: any read outside the support would poison the result
             states[w][:] = np.nan
         sp_of.append(sp)
@@ -249,12 +257,16 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
             for w, (geo, dp, descs, p) in enumerate(progs):
                 sw = {s.task_id: s for s in dp.steps}[task.id]
                 run_sweeps(states[w], descs[sw.first: sw.first + sw.count], p, norms,
-                           [sp_of[w].get(i) for i in range(sw.first, sw.first + sw.count)])
+                           [sp_of[w].get(i) for i in range(sw.first, sw.first + sw.count)],
+                           [lx_of[w].get(i) for i in range(sw.first, sw.first + sw.count)])
             if st.count == 0 and slot not in progs[0][1].norm_alias:
                 norms[slot] = norms[slot - 1] if slot else 1.0  # |0...0> (maybe not materialised yet)
         elif task.kind == "Exchange" and st.kind == "localize":
             # every device moves region alpha (its id bits) of its replica to region 0
+            # (unless the next sweep reads it through a load XOR)
             for w in range(world):
+                if {s_.task_id: s_ for s_ in progs[w][1].steps}[task.id].folded:
+                    continue
                 me = w
                 alpha, lbs = 0, []
                 for ib, lb in st.swaps:
@@ -287,7 +299,8 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
     if mat is not None:
         for w, (geo, dp, descs, p) in enumerate(progs):
             run_sweeps(states[w], descs[mat.first: mat.first + mat.count], p, None,
-                       [sp_of[w].get(i) for i in range(mat.first, mat.first + mat.count)])
+                       [sp_of[w].get(i) for i in range(mat.first, mat.first + mat.count)],
+                       [lx_of[w].get(i) for i in range(mat.first, mat.first + mat.count)])
     blocks = np.concatenate([s[: rows << L] for s in states]).reshape(nr, 1 << L)
     alias = progs[0][1].norm_alias
     norms = np.array([norms[alias.get(i, i)] for i in range(len(norms))])

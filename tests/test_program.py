@@ -115,8 +115,9 @@ def test_stable_thread_orders():
 
 
 
-@pytest.mark.parametrize("world,kmax", [(2, 12), (4, 12), (2, 6), (4, 7), (8, 12)])
-def test_localized_first_remap_matches_reference(grid_docs, grid_states, world, kmax):
+@pytest.mark.parametrize("world,kmax,fold", [(2, 12, True), (4, 12, True), (2, 6, True), (4, 7, True),
+                                             (8, 12, True), (2, 6, False), (4, 7, False)])
+def test_localized_first_remap_matches_reference(grid_docs, grid_states, world, kmax, fold):
     """Runs from |0...0> whose first remap follows only sparse sweeps: every
     device computes the prefix as the unit-holding device and the remap is
     a local region move (program.localize_applies)."""
@@ -125,7 +126,7 @@ def test_localized_first_remap_matches_reference(grid_docs, grid_states, world, 
     n = used = 0
     for doc in _cases(grid_docs, grid_states, min_ranks=world):
         plan = plan_from_doc(doc["plan"])
-        blocks, norms = program_emu.emulate_plan(plan, world=world, sparse=True, kmax=kmax, localize=True)
+        blocks, norms = program_emu.emulate_plan(plan, world=world, sparse=True, kmax=kmax, localize=True, fold=fold)
         err = float(np.max(np.abs(blocks - grid_states[doc["name"]])))
         assert err < TOL, (doc["name"], world, err)
         assert np.all(np.abs(norms - 1) < 1e-8), doc["name"]
