@@ -25,7 +25,6 @@ There is no CPU execution path: without the CUDA library every call raises.
 
 from __future__ import annotations
 
-import math
 import os
 from dataclasses import dataclass, field
 

@@ -31,7 +31,6 @@ virtual (relabel / flip the tile bit and fix it up in the store mapping).
 
 from __future__ import annotations
 
-import cmath
 import math
 from dataclasses import dataclass, field
 

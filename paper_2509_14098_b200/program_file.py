@@ -20,7 +20,6 @@ through include/svb200.h and checks the norms.
 
 from __future__ import annotations
 
-import json
 import struct
 from pathlib import Path
 

@@ -1,7 +1,7 @@
 """Layout kernel throughput on one GPU: out-of-place storage<->basis bit
 permutations (svb_bitperm: gather/scatter) and in-place bit swaps
 (svb_bitswap: initial-state layouts), on 2^30 amplitudes.  Prints JSON."""
-import ctypes
+
 import json
 import sys
 from pathlib import Path

@@ -11,7 +11,7 @@ sys.path.insert(0, str(ROOT))
 
 import torch  # noqa: E402
 
-from paper_2509_14098_b200 import executor, plan as planmod, run_plan  # noqa: E402
+from paper_2509_14098_b200 import plan as planmod, run_plan  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "qv30_h30-12"
 plan = planmod.load(str(ROOT / "plans" / f"{name}.json.gz"))
