@@ -618,6 +618,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
 
 
 GROUP_OFFSET = os.environ.get("SVB200_JIT_GROUP_OFFSET", "1") not in ("0", "false", "no")
+GROUPS_ONLY = int(os.environ["SVB200_JIT_GROUPS_ONLY"]) if os.environ.get("SVB200_JIT_GROUPS_ONLY") else None
 SKIP_DEAD = os.environ.get("SVB200_JIT_SKIP_DEAD", "1") not in ("0", "false", "no")
 # sweeps whose FP64 work per amplitude reaches this many DFMA (a fused 4x4 is
 # 16) run two tile groups per CTA (kernel_source_2g)
@@ -1202,6 +1203,8 @@ def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: in
             used[i] = zi
         two = (GROUPS and not d.get("cbits") and (1 << (int(d["K"]) - int(d["rb"]))) == 256
                and dfma_per_amp(ops, int(d["rb"])) >= GROUPS_MIN_DFMA)
+        if GROUPS_ONLY is not None:  # debugging: two groups for one descriptor only
+            two = i == GROUPS_ONLY and not d.get("cbits")
         gen = kernel_source_2g if two else kernel_source
         if two:
             groups[i] = 2
