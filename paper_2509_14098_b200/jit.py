@@ -709,7 +709,7 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
       "const u64 part_val, const u64 part_tid, const long long ntiles) {")
     w("  extern __shared__ __align__(16) double2 smem[];")
     w("  __shared__ double red[32];")
-    w("  __shared__ __align__(8) unsigned long long mbar[3];")
+    w("  __shared__ __align__(8) unsigned long long mbar[6];")
     w(f"  const int grp = threadIdx.x >> {tb};")
     w(f"  const int t = threadIdx.x & {NT - 1};")
     w("  const u32 bar_id = 1u + (u32)grp;")
@@ -784,7 +784,7 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
                 w(f"      cp_async16({buf} + (lds_t ^ {s_}u), state + chk({base} | ld_t | {dev}ull));")
 
     w("  if (threadIdx.x == 0) {")
-    w("    for (int b = 0; b < 3; ++b) mbar_init(&mbar[b], " + str(NT) + "u);")
+    w("    for (int b = 0; b < 6; ++b) mbar_init(&mbar[b], " + str(NT) + "u);")
     w("    mbar_init_fence();")
     w("  }")
     w("  __syncthreads();")
@@ -834,7 +834,7 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
         w("      ctab[i] = acc;")
         w("    } }")
     if not zero_init:
-        w("    mbar_wait_parity(&mbar[b], (u32)((k / 3) & 1));")
+        w("    mbar_wait_parity(&mbar[k % 6], (u32)((k / 6) & 1));")
     w(f"    bar_group(bar_id, {NT}u);")
     w(f"    double2 x[{NR}];")
     cur = None
@@ -894,7 +894,7 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
         w(f"        const u64 bn = {origin('nk')};")
         prefetch_items("tile", "bn")
         w("      }")
-        w("      cp_async_mbar_arrive(&mbar[b]);")
+        w("      cp_async_mbar_arrive(&mbar[(k + 3) % 6]);")
         w("    }")
     w("  }")
     if mid is not None:  # group 0 had no tile: release group 1
