@@ -650,9 +650,15 @@ def kernel_source_2g(name: str, desc: dict, ops: list, coef: list, zero_init: in
     of the CTA's sequence (tile k -> group k % 2, buffer k % 3), each with
     its own named barrier, so one group's stages and stores run while the
     other computes.  Loads are cp.async into the buffer of tile k+3, issued
-    by the group that just stored tile k from that buffer and tracked by a
-    per-buffer mbarrier (cp.async.mbarrier.arrive) that the consuming group
-    waits on with the phase parity of the buffer's use.  Registers: 512
+    by the group that just stored tile k from that buffer and tracked by an
+    mbarrier per tile index mod 6 (cp.async.mbarrier.arrive): the consumer
+    of tile k waits on barrier k mod 6 with parity (k / 6) & 1.  Six
+    barriers, not one per buffer: a parity wait cannot tell phase j from
+    phase j - 2, and with one barrier per buffer a consumer could reach
+    tile k + 3 while the loads of tile k were still in flight and take
+    them as complete (found on light QFT sweeps, tools/kernel_ab.py);
+    barrier k mod 6 was last waited on by the same group for tile k - 6,
+    so its previous phase is always complete.  Registers: 512
     threads leave 128 per thread."""
     K, D = desc["K"], desc["D"]
     rb = int(desc["rb"])
