@@ -38,9 +38,8 @@ NO_AHEAD_ZERO = os.environ.get("SVB200_JIT_NO_AHEAD_ZERO", "1") not in ("0", "fa
 # stage changes that keep the warp-level thread bits move data with warp shuffles
 SHUFFLE_STAGES = os.environ.get("SVB200_JIT_SHUFFLE", "0") not in ("0", "false", "no")  # measured: slower
 # FP64-heavy sweeps can run two tile groups per CTA (kernel_source_2g,
-# SVB200_JIT_GROUPS=1).  Off by default: it gained 2-4% on QV-30, and forcing
-# it onto every sweep (SVB200_JIT_GROUPS_MIN_DFMA=0) exposed wrong norms on
-# phase-table QFT sweeps and a stall on a sparse one (round 2, unresolved)
+# SVB200_JIT_GROUPS=1).  Off by default: QV-30 moved between -6% and +4%
+# across boxes
 GROUPS = os.environ.get("SVB200_JIT_GROUPS", "0") not in ("0", "false", "no")
 NVRTC_OPTS = ["--gpu-architecture=sm_100a", "--std=c++17", f"-I{CSRC}", "-lineinfo",
               "--extra-device-vectorization"]
