@@ -512,6 +512,8 @@ def main() -> None:
                      "bytes_per_launch": dom_bytes, "launch_ms": dom_ms, "share_of_sweep_time": dom_share,
                      "bytes_note": "HBM bytes the launch must move: 16 B per amplitude read + 16 B per "
                                    "amplitude written (sparse |0...0>-start sweeps read only the support)",
+                     "per_sweep_ms": {str(di): round(sum(t for _, t in lst) / len(lst), 4)
+                                      for di, lst in sorted(acc["prof"].items())},
                      "all_sweeps": {"achieved": all_achieved, "frac": all_achieved / peak,
                                     "bytes_per_step": acc["sweep_bytes"] // args.steps,
                                     "launches_per_step": sweeps // args.steps,
