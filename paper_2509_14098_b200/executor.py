@@ -259,7 +259,9 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
         unit = geo.rank_base == 0 or any(st.kind == "localize" for st in dp.steps)  # replicas hold it too
         sparse = prog.sparse_start(dp, geo.D, unit) if (zero_start and SPARSE_START) else {}
         ld_xor = _fold_localize(dp, geo, sparse)
-        names, slots = jitmod.build_kernels(dp.buf, sparse=sparse, lazy=PIPELINED_JIT, ld_xor=ld_xor)
+        st_keep = _prefix_store_masks(dp, geo, sparse)
+        names, slots = jitmod.build_kernels(dp.buf, sparse=sparse, lazy=PIPELINED_JIT, ld_xor=ld_xor,
+                                            st_keep=st_keep)
         out.zero_init = dict(jitmod._LAST_ZERO_INIT)
         out.sparse = sparse
         for i, gcount in jitmod._LAST_GROUPS.items():  # launch geometry of two-group kernels
@@ -1072,6 +1074,35 @@ def _fold_localize(dp, geo: prog.DeviceGeometry, sparse: dict) -> dict:
         if mask:
             out[nxt.first] = mask
         st.folded = True
+    return out
+
+
+def _prefix_store_masks(dp, geo: prog.DeviceGeometry, sparse: dict) -> dict:
+    """The last sweep of a replicated prefix stores only this process's
+    region alpha of the swapped local bits when those bits are its tile bits
+    (the other regions are never read again): {descriptor: (mask, value)}."""
+    out = {}
+    steps = dp.steps
+    for i, st in enumerate(steps):
+        if st.kind != "localize":
+            continue
+        prev = next((x for x in reversed(steps[:i]) if x.kind in ("sweeps", "materialize") and x.count), None)
+        if prev is None:
+            continue
+        di = prev.first + prev.count - 1
+        d = dp.buf.descs[di]
+        if di not in sparse or sparse[di][1]:  # full_out sweeps write every position
+            continue
+        tin = set(int(b) for b in d["tin"][:d["K"]])
+        if not all(lb in tin for _, lb in st.swaps):
+            continue
+        alpha, m = _alpha(st, geo), len(st.swaps)
+        mask = val = 0
+        for j, (_, lb) in enumerate(st.swaps):
+            mask |= 1 << lb
+            if (alpha >> (m - 1 - j)) & 1:
+                val |= 1 << lb
+        out[di] = (mask, val)
     return out
 
 

@@ -162,8 +162,13 @@ def _warp_local_change(stage_info: list, a: int, b: int, nthreads: int) -> bool:
 
 
 def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int = 0,
-                  sparse: tuple | None = None, ld_xor: int = 0) -> str:
+                  sparse: tuple | None = None, ld_xor: int = 0, st_keep: tuple | None = None) -> str:
     """Straight-line kernel for one sweep.
+
+    st_keep = (mask, value): only positions whose tile bits at `mask` read
+    `value` are stored (the last sweep of a replicated prefix: the localized
+    remap keeps only this process's region).  The norm still covers every
+    amplitude of the tile.
 
     ld_xor: tile bits XOR-ed into every load address (the first sweep after a
     localized remap reads region alpha of the swapped bits as region 0; the
@@ -362,7 +367,12 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
             w("      {")
             w(f"        const double2 v = {buf}[sts_t ^ {s}u];")
             w("        nrm = fma(v.x, v.x, fma(v.y, v.y, nrm));")
-            w(f"        st_stream(state + chk({base} | ((st_t | {dev}ull) ^ {st_flip}ull)), v);")
+            if st_keep is None:
+                w(f"        st_stream(state + chk({base} | ((st_t | {dev}ull) ^ {st_flip}ull)), v);")
+            else:
+                km, kv = st_keep
+                w(f"        if (((st_t ^ {dev ^ st_flip}ull) & {km}ull) == {kv}ull)")
+                w(f"          st_stream(state + chk({base} | ((st_t | {dev}ull) ^ {st_flip}ull)), v);")
             w("      }")
 
     def slot(j):
@@ -1183,7 +1193,7 @@ def _nvrtc(src: str, name: str, h: str) -> bytes:
 
 def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: int | None = None,
                   zero_init: dict | None = None, sparse: dict | None = None, lazy: bool = False,
-                  ld_xor: dict | None = None):
+                  ld_xor: dict | None = None, st_keep: dict | None = None):
     """Generate + compile one kernel per sweep descriptor; returns (names, cubins).
 
     zero_init maps descriptor index -> 1/2 for sweeps whose input is known to
@@ -1213,10 +1223,11 @@ def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: in
         gen = kernel_source_2g if two else kernel_source
         if two:
             groups[i] = 2
-        if (ld_xor or {}).get(i):
-            gen = kernel_source  # the one-group kernel carries the load XOR
+        if (ld_xor or {}).get(i) or (st_keep or {}).get(i):
+            gen = kernel_source  # the one-group kernel carries the load XOR / store mask
             groups.pop(i, None)
-            body = gen("KNAME", d, ops, buf.coef, zi, sparse.get(i), ld_xor[i])
+            body = gen("KNAME", d, ops, buf.coef, zi, sparse.get(i), (ld_xor or {}).get(i, 0),
+                       (st_keep or {}).get(i))
         else:
             body = gen("KNAME", d, ops, buf.coef, zi, sparse.get(i))
         h = hashlib.sha1(body.encode()).hexdigest()[:16]

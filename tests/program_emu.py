@@ -31,7 +31,7 @@ def _xor_img(vals: np.ndarray, imgs) -> np.ndarray:
 
 
 def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None, sparse=None,
-               ld_xor=None) -> None:
+               ld_xor=None, st_keep=None) -> None:
     """In-place on the flat device state (length 2^D).
 
     sparse: per descriptor (support, full_out) or None (program.sparse_start);
@@ -43,6 +43,7 @@ def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None,
     for di, d in enumerate(descs):
         sp = sparse[di] if sparse is not None else None
         lx = (ld_xor[di] or 0) if ld_xor is not None else 0
+        keep = st_keep[di] if st_keep is not None else None
         K, D = int(d["K"]), int(d["D"])
         RB = int(d["rb"])
         NR = 1 << RB
@@ -183,7 +184,11 @@ def run_sweeps(state: np.ndarray, descs, parts, norms: np.ndarray | None = None,
                 tile[J] = x
             vals = tile[st_s]
             nrm += float(np.sum(np.abs(vals) ** 2))
-            state[base | st_d] = vals
+            if keep is None:
+                state[base | st_d] = vals
+            else:  # only this process's region of a localized remap is stored
+                sel = ((base | st_d) & keep[0]) == keep[1]
+                state[(base | st_d)[sel]] = vals[sel]
         slot = int(d["norm_slot"])
         if norms is not None and slot >= 0:
             norms[slot] += nrm
@@ -236,15 +241,17 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
                 [(s.kind, s.task_id, s.swaps) for s in progs[0][1].steps]
     states = [np.zeros(1 << D, dtype=np.complex128) for _ in range(world)]
     states[0][0] = 1.0
-    sp_of, lx_of = [], []  # per device: descriptor -> (support, full_out); descriptor -> load XOR
+    sp_of, lx_of, keep_of = [], [], []  # per device: descriptor -> (support, full_out) / load XOR / store mask
     for w, (geo, dp, descs, p) in enumerate(progs):
         sp = prog.sparse_start(dp, D, w == 0 or replicate) if sparse else {}
         if replicate and fold:
-            from paper_2509_14098_b200.executor import _fold_localize
+            from paper_2509_14098_b200.executor import _fold_localize, _prefix_store_masks
 
             lx_of.append(_fold_localize(dp, geo, sp))
+            keep_of.append(_prefix_store_masks(dp, geo, sp))
         else:
             lx_of.append({})
+            keep_of.append({})
         if sp:  # unwritten memory: any read outside the support would poison the result
             states[w][:] = np.nan
         sp_of.append(sp)
@@ -258,7 +265,8 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
                 sw = {s.task_id: s for s in dp.steps}[task.id]
                 run_sweeps(states[w], descs[sw.first: sw.first + sw.count], p, norms,
                            [sp_of[w].get(i) for i in range(sw.first, sw.first + sw.count)],
-                           [lx_of[w].get(i) for i in range(sw.first, sw.first + sw.count)])
+                           [lx_of[w].get(i) for i in range(sw.first, sw.first + sw.count)],
+                           [keep_of[w].get(i) for i in range(sw.first, sw.first + sw.count)])
             if st.count == 0 and slot not in progs[0][1].norm_alias:
                 norms[slot] = norms[slot - 1] if slot else 1.0  # |0...0> (maybe not materialised yet)
         elif task.kind == "Exchange" and st.kind == "localize":
