@@ -180,6 +180,16 @@ class ClockSampler:
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+        # nvidia-smi takes a moment to start: begin the timed region only once
+        # it is sampling, so its samples cover the (short) timed region
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < 3.0:
+            try:
+                if self.out.stat().st_size > 0:
+                    break
+            except OSError:
+                pass
+            time.sleep(0.02)
         return self
 
     def __exit__(self, *exc):
