@@ -1216,6 +1216,76 @@ def unpack_order(val: int, n: int) -> list:
     return [(int(val) >> (4 * i)) & 15 for i in range(n)]
 
 
+STAGE_SCHED = os.environ.get("SVB200_STAGE_SCHED", "1") not in ("0", "false", "no")
+
+
+def _touched(it, tin: list) -> set:
+    """Physical device bits an item reads or writes (targets, controls, phases)."""
+    out = {tin[k] for k in it.bits}
+    out |= set(it.ctrl)
+    for f in it.factors:
+        out |= set(f.bits)
+    return out
+
+
+def _stages_sched(items: list, rb: int, tin: list) -> list:
+    """Stages by list scheduling: items that touch disjoint bits commute, so
+    a stage may take any item whose predecessors on its bits are scheduled
+    and whose register bits fit the stage.  Each stage starts from the ready
+    item that lets the most items join it.  Fewer stages = fewer shared-
+    memory round trips per tile (a stage moves the whole 64 KB tile)."""
+    n = len(items)
+    touched = [_touched(it, tin) for it in items]
+    preds = [set() for _ in range(n)]
+    last: dict = {}
+    for i in range(n):
+        for b in touched[i]:
+            if b in last:
+                preds[i].add(last[b])
+        for b in touched[i]:
+            last[b] = i
+    done = [False] * n
+    left = n
+    stages = []
+
+    def grow(seed_bits: set, seed_order: list) -> tuple:
+        need, order = set(seed_bits), list(seed_order)
+        taken = set(order)
+        while True:  # add the fitting ready item that needs the fewest new register bits
+            pick, cost = None, None
+            for i in range(n):
+                if done[i] or i in taken or not all(done[p] or p in taken for p in preds[i]):
+                    continue
+                nb = set(items[i].bits)
+                if len(need | nb) > rb:
+                    continue
+                c = len(nb - need)
+                if cost is None or c < cost:
+                    pick, cost = i, c
+                    if c == 0:
+                        break
+            if pick is None:
+                return need, order
+            need |= set(items[pick].bits)
+            order.append(pick)
+            taken.add(pick)
+
+    while left:
+        ready = [i for i in range(n) if not done[i] and all(done[p] for p in preds[i])]
+        best = None
+        for r in ready[:24]:  # seeds: the first ready items (bounded work per stage)
+            need, order = grow(set(items[r].bits), [r])
+            if best is None or len(order) > len(best[1]):
+                best = (need, order)
+        need, order = best
+        order.sort()  # program order inside the stage (dependencies hold)
+        for i in order:
+            done[i] = True
+        left -= len(order)
+        stages.append([need, [items[i] for i in order]])
+    return stages
+
+
 def _stages(items: list, rb: int = RB) -> list:
     """Group items into stages of <= rb register bits; returns [(rbits, items)]."""
     stages = []
@@ -1266,7 +1336,8 @@ def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers, rb: i
     # fold the accumulated constant / H scale into the final phase item
     final = items[-1]
     assert final.kind == OP_PHALL
-    stages = _stages([it for it in items if it.kind != OP_PHALL], rb)
+    body = [it for it in items if it.kind != OP_PHALL]
+    stages = _stages_sched(body, rb, tin) if STAGE_SCHED else _stages(body, rb)
     if not stages and (final.factors or sp.scale != 1):
         stages = [[set(), []]]
     # pad register sets to exactly rb bits, preferring bits used soon after
