@@ -286,12 +286,27 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     # tile is stored straight from shared memory and needs the zero fill
     skip_dead = SKIP_DEAD and bool(ld_zero) and bool(stage_info)
     zk = {k for k in range(K) if (ld_zero >> tin[k]) & 1}
+    # tile bits (indices into tin) that may be 1 at a nonzero amplitude: the
+    # support inside the tile, grown by the ops that mix a dead bit in
+    # (_emit_op zm); all bits of a |0...0> start are dead
+    track = ZERO_TRACK and not SPLIT_STAGES and (bool(ld_zero) or bool(zero_init))
+    live = set(range(K)) if not track else (set() if zero_init else set(range(K)) - zk)
+
+    def zmask(si):
+        return sum(1 << q for q, k in enumerate(stage_info[si][0]) if k not in live)
+
+    def tdead(si):  # thread bits on dead tile bits: such a thread holds zeros only
+        return sum(1 << i for i, k in enumerate(stage_info[si][1]) if k not in live)
 
     def emit_stage_read(si, offs):
         regs, comp, _ = stage_info[si]
         if si != 0 or not skip_dead:
+            zm = zmask(si)
             for v in range(NR):
-                w(f"    x[{v}] = tile[sb{si} ^ {offs[v]}u];")
+                if v & zm:
+                    w(f"    x[{v}] = make_double2(0.0, 0.0);")
+                else:
+                    w(f"    x[{v}] = tile[sb{si} ^ {offs[v]}u];")
             return
         tmask = sum(1 << i for i, k in enumerate(comp) if k in zk)
         if tmask:
@@ -462,8 +477,25 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     pending = []  # ops since the last stage
 
     def flush(half=None):
+        if not track or cur is None or half is not None:
+            for o in pending:
+                _emit_op(w, o, coef, cur, K, rb, half)
+            return
+        td = tdead(cur)
+        if td and pending:  # ops are linear in the thread's own registers
+            w(f"    if ((t & {td}u) == 0u) {{")
         for o in pending:
-            _emit_op(w, o, coef, cur, K, rb, half)
+            woke = _emit_op(w, o, coef, cur, K, rb, None, zmask(cur))
+            live.update(stage_info[cur][0][q] for q in range(rb) if (woke >> q) & 1)
+        if td and pending:
+            w("    }")
+
+    def store_regs(si):
+        zm = zmask(si)
+        _, _, offs = stage_info[si]
+        for v in range(NR):
+            val = "make_double2(0.0, 0.0)" if v & zm else f"x[{v}]"
+            w(f"    tile[sb{si} ^ {offs[v]}u] = {val};")
 
     def split_slot(a_stage, b_stage):
         """A register slot whose tile bit stays a register bit across the stage
@@ -555,8 +587,11 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                 halves = [None] if q is None else [(q, 0), (q, 1)]
                 for hf in halves:
                     flush(hf)
+                    if hf is None:
+                        store_regs(cur)
+                        continue
                     for v in range(NR):
-                        if hf is None or ((v >> q) & 1) == hf[1]:
+                        if ((v >> q) & 1) == hf[1]:
                             w(f"    tile[sb{cur} ^ {offs[v]}u] = x[{v}];")
                 w("    __syncwarp();" if _warp_local_change(stage_info, cur, nxt, NT) else "    __syncthreads();")
             else:
@@ -579,9 +614,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     pending = []
 
     if cur is not None:
-        _, _, offs = stage_info[cur]
-        for v in range(NR):
-            w(f"    tile[sb{cur} ^ {offs[v]}u] = x[{v}];")
+        store_regs(cur)
     if ahead:  # the next tile's slots, from loads issued at the start of this one
         nch = int(desc["lut_nch"])
         w(f"    if (has_next && t < {nct}) {{")
@@ -629,6 +662,8 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
 GROUP_OFFSET = os.environ.get("SVB200_JIT_GROUP_OFFSET", "1") not in ("0", "false", "no")
 GROUPS_ONLY = int(os.environ["SVB200_JIT_GROUPS_ONLY"]) if os.environ.get("SVB200_JIT_GROUPS_ONLY") else None
 SKIP_DEAD = os.environ.get("SVB200_JIT_SKIP_DEAD", "1") not in ("0", "false", "no")
+# sparse sweeps: known-zero registers drop out of the arithmetic (kernel_source)
+ZERO_TRACK = os.environ.get("SVB200_JIT_ZERO_TRACK", "1") not in ("0", "false", "no")
 # sweeps whose FP64 work per amplitude reaches this many DFMA (a fused 4x4 is
 # 16) run two tile groups per CTA (kernel_source_2g)
 GROUPS_MIN_DFMA = float(os.environ.get("SVB200_JIT_GROUPS_MIN_DFMA", "48"))
@@ -975,21 +1010,33 @@ def _phase_base(w, op, coef_c0: complex, K: int, rb: int) -> None:
             w(f"      if ((t >> {i}) & 1) p = cmul(p, ctab[{int(op['tf']) + i}]);")
 
 
-def _emit_op(w, op, coef, stage, K, rb, half=None) -> None:
+def _emit_op(w, op, coef, stage, K, rb, half=None, zm: int = 0) -> int:
     """Emit one op; `half` = (register slot, value) restricts it to the
     amplitudes whose slot bit has that value (ops that do not pair across
-    that slot split exactly into two halves)."""
+    that slot split exactly into two halves).
+
+    zm: register slots whose tile bit is still dead (register v holds an
+    exact zero whenever v & zm; kernel_source tracks this from the sparse
+    support).  Terms on such registers are dropped: a butterfly with a zero
+    partner becomes a copy, a phase on a zero amplitude is skipped.  Every
+    dropped term is an exact zero added or multiplied, so the results equal
+    the full computation's (up to the sign of zero).  Returns the slots the
+    op makes live."""
     NR = 1 << rb
     kind = int(op["kind"])
 
     def skip(v):
         return half is not None and ((v >> half[0]) & 1) != half[1]
 
+    def z(v):
+        return bool(v & zm)
+
     a = int(op["a"])
     A = 1 << a
     cm, cv = int(op["rmask"]), int(op["b"])
     cf = int(op["coef"])
     pmask, pval = int(op["pmask"]), int(op["pval"])
+    woke = 0
     w("    {")
     if pmask:
         w(f"    if (((base | db{stage}) & {pmask}ull) == {pval}ull) {{")
@@ -1001,26 +1048,46 @@ def _emit_op(w, op, coef, stage, K, rb, half=None) -> None:
             _phase_base(w, op, coef[ph], K, rb)
             nt = (int(op["flags"]) >> prog.F_PREG_SHIFT) & 0xF
             fused = kind == prog.OP_H and cm == 0
-            _emit_dfs(w, a, nt, [coef[ph + 1 + s] for s in range(rb)], fused, rb, half)
+            _emit_dfs(w, a, nt, [coef[ph + 1 + s] for s in range(rb)], fused, rb, half, zm)
         if kind == prog.OP_H and not fused:
             for v in range(NR):
                 if (v & A) or (v & cm) != cv or skip(v):
                     continue
-                w(f"      {{ const double2 x0 = x[{v}], x1 = x[{v | A}]; "
-                  f"x[{v}] = cadd(x0, x1); x[{v | A}] = csub(x0, x1); }}")
+                z0, z1 = z(v), z(v | A)
+                if z0 and z1:
+                    continue
+                if z1:
+                    w(f"      x[{v | A}] = x[{v}];")
+                elif z0:
+                    w(f"      x[{v}] = x[{v | A}]; x[{v | A}] = make_double2(-x[{v}].x, -x[{v}].y);")
+                else:
+                    w(f"      {{ const double2 x0 = x[{v}], x1 = x[{v | A}]; "
+                      f"x[{v}] = cadd(x0, x1); x[{v | A}] = csub(x0, x1); }}")
         elif kind == prog.OP_U1:
             m00, m01, m10, m11 = coef[cf:cf + 4]
             for v in range(NR):
                 if (v & A) or (v & cm) != cv or skip(v):
                     continue
+                z0, z1 = z(v), z(v | A)
+                if z0 and z1:
+                    continue
+                t0 = [] if z0 else [(m00, "x0")]
+                t1 = [] if z0 else [(m10, "x0")]
+                if not z1:
+                    t0.append((m01, "x1"))
+                    t1.append((m11, "x1"))
                 w(f"      {{ const double2 x0 = x[{v}], x1 = x[{v | A}]; "
-                  f"x[{v}] = {_lincomb([(m00, 'x0'), (m01, 'x1')])}; "
-                  f"x[{v | A}] = {_lincomb([(m10, 'x0'), (m11, 'x1')])}; }}")
+                  f"x[{v}] = {_lincomb(t0)}; x[{v | A}] = {_lincomb(t1)}; }}")
+        if kind in (prog.OP_H, prog.OP_U1):
+            woke |= A
     elif kind == prog.OP_X:
         for v in range(NR):
             if (v & A) or (v & cm) != cv or skip(v):
                 continue
+            if z(v) and z(v | A):
+                continue
             w(f"      {{ const double2 tmp = x[{v}]; x[{v}] = x[{v | A}]; x[{v | A}] = tmp; }}")
+        woke |= A  # the zero half moves to bit value 0: no longer "bit set -> zero"
     elif kind == prog.OP_U2:
         b = int(op["b"])
         B = 1 << b
@@ -1029,37 +1096,51 @@ def _emit_op(w, op, coef, stage, K, rb, half=None) -> None:
             if (v & A) or (v & B) or skip(v):
                 continue
             idx = [v, v | B, v | A, v | A | B]
+            live = [c for c in range(4) if not z(idx[c])]
+            if not live:
+                continue
             w("      {")
-            w(f"        const double2 a0 = x[{idx[0]}], a1 = x[{idx[1]}], a2 = x[{idx[2]}], a3 = x[{idx[3]}];")
+            w("        const double2 " + ", ".join(f"a{c} = x[{idx[c]}]" for c in live) + ";")
             for r in range(4):
-                w(f"        x[{idx[r]}] = {_lincomb([(M[r, c], f'a{c}') for c in range(4)])};")
+                w(f"        x[{idx[r]}] = {_lincomb([(M[r, c], f'a{c}') for c in live])};")
             w("      }")
+        woke |= A | B
     elif kind == prog.OP_PHALL:
         _phase_base(w, op, coef[cf], K, rb)
         for v in range(NR):
-            if not skip(v):
+            if not skip(v) and not z(v):
                 w(f"      x[{v}] = cmul(x[{v}], p);")
     elif kind == prog.OP_SCALE:
         for v in range(NR):
-            if not skip(v):
+            if not skip(v) and not z(v):
                 w(f"      x[{v}] = {_cmul_lit(f'x[{v}]', coef[cf])};")
     if pmask:
         w("    }")
     w("    }")
+    return woke & zm
 
 
-def _emit_dfs(w, a: int, nt: int, c: list, fused_h: bool, rb: int, half=None) -> None:
-    """Depth-first product over register slots != a; leaves are amplitudes with bit a set."""
+def _emit_dfs(w, a: int, nt: int, c: list, fused_h: bool, rb: int, half=None, zm: int = 0) -> None:
+    """Depth-first product over register slots != a; leaves are amplitudes with bit a set
+    (zm: see _emit_op; unused partial products are dead code)."""
     counter = [0]
 
     def rec(s, v, pv):
         if s == rb:
             if half is not None and ((v >> half[0]) & 1) != half[1]:
                 return  # the other half (unused partial products are dead code)
+            u = v ^ (1 << a)
             if fused_h:
-                w(f"      {{ const double2 x1 = cmul(x[{v}], {pv}); const double2 x0 = x[{v ^ (1 << a)}]; "
-                  f"x[{v ^ (1 << a)}] = cadd(x0, x1); x[{v}] = csub(x0, x1); }}")
-            else:
+                if v & zm and u & zm:
+                    return
+                if v & zm:  # x1 = 0: both outputs are x0
+                    w(f"      x[{v}] = x[{u}];")
+                elif u & zm:  # x0 = 0
+                    w(f"      x[{u}] = cmul(x[{v}], {pv}); x[{v}] = make_double2(-x[{u}].x, -x[{u}].y);")
+                else:
+                    w(f"      {{ const double2 x1 = cmul(x[{v}], {pv}); const double2 x0 = x[{u}]; "
+                      f"x[{u}] = cadd(x0, x1); x[{v}] = csub(x0, x1); }}")
+            elif not v & zm:
                 w(f"      x[{v}] = cmul(x[{v}], {pv});")
             return
         if s == a:
