@@ -50,6 +50,7 @@ FALLBACK_HBM = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 E2E_HOST_BYTES = 48 << 30  # pinned host buffers per process (in and out each)
 TRAFFIC_REV = "r02"  # profiles/traffic.json entries measured on the current sweep code
 E2E_PIPELINE = os.environ.get("SVB200_E2E_PIPELINE", "1") != "0"  # two circuits in flight
+PIPELINE = os.environ.get("SVB200_BENCH_PIPELINE", "1") != "0"  # timed loop: two circuits in flight when they fit
 
 
 def workload_name(kind: str, n: int) -> tuple[str, str]:
@@ -337,11 +338,31 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # each result is dropped before the next run: its state buffer returns to
-    # the pool (at 34 qubits on 2 GPUs one state is 128 GiB of the 180)
-    for _ in range(args.warmup):
-        res = run_plan(plan)
-        del res
+    def in_flight(plan_) -> int:
+        """2 when two copies of this process's state fit in half the device memory."""
+        state_bytes = 16 * ((1 << plan_.g) // world) << (plan_.d - plan_.g)
+        total = torch.cuda.get_device_properties(local).total_memory
+        return 2 if PIPELINE and 2 * state_bytes <= total // 2 else 1
+
+    def warm(plan_, n):
+        """Untimed runs in the timed loop's pattern (so the second in-flight
+        state buffer exists before the clock starts).  Otherwise each result
+        is dropped before the next run: its state buffer returns to the pool
+        (at 34 qubits on 2 GPUs one state is 128 GiB of the 180)."""
+        two = in_flight(plan_) == 2
+        prev = None
+        for _ in range(n):
+            r = run_plan(plan_, wait=not two)
+            if prev is not None:
+                prev.wait()
+            prev = r if two else None
+            del r
+        if prev is not None:
+            prev.wait()
+        del prev
+        torch.cuda.synchronize()
+
+    warm(plan, args.warmup)
     barrier()
 
     def timed(plan_, steps, clk_=None):
@@ -350,10 +371,9 @@ def main() -> None:
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         acc = {"compute_s": 0.0, "launches": 0, "sweeps": 0, "sweep_bytes": 0, "prof": {}}
         executor.PROFILE_SWEEPS = True
-        barrier()
-        start.record()
-        for _ in range(steps):
-            r = run_plan(plan_)
+
+        def collect(r):
+            r.wait()  # event timings and the drift check of that circuit
             acc["compute_s"] += r.stats.compute_seconds + r.stats.layout_seconds
             acc["launches"] += r.stats.kernel_launches
             acc["sweeps"] += r.stats.sweeps
@@ -361,7 +381,26 @@ def main() -> None:
             for di, lst in r.stats.sweep_profile.items():
                 acc["prof"].setdefault(di, []).extend(lst)
             acc["stats"] = r.stats
+
+        inflight = in_flight(plan_)
+        barrier()
+        start.record()
+        prev = None
+        for _ in range(steps):
+            # with two circuits in flight the host enqueues circuit i+1 while
+            # the GPU runs circuit i (every circuit is still computed and
+            # drift-checked in full)
+            r = run_plan(plan_, wait=inflight == 1)
+            if prev is not None:
+                collect(prev)
+            prev = r
+            if inflight == 1:
+                collect(r)
+                prev = None
             del r
+        if prev is not None:
+            collect(prev)
+        del prev
         stop.record()
         barrier()
         executor.PROFILE_SWEEPS = False
@@ -444,9 +483,7 @@ def main() -> None:
     subs = {}
     if world == 1 and args.workload == "qft" and args.sub_steps > 0:
         executor.SPARSE_START = False
-        for _ in range(3):
-            del_ = run_plan(plan)
-            del del_
+        warm(plan, 3)
         a2 = timed(plan, args.sub_steps)
         executor.SPARSE_START = True
         subs["dense_passes"] = {
@@ -474,6 +511,7 @@ def main() -> None:
         first_run_s = time.perf_counter() - t0
         jitmod.CACHE_DIR = saved
         del del_
+        warm(qvp, 2)
         a3 = timed(qvp, max(1, args.sub_steps // 3))
         k3 = max(1, args.sub_steps // 3)
         di3, b3, ms3, sh3 = dominant(a3["prof"])
@@ -511,7 +549,8 @@ def main() -> None:
                    "l2": f"state {16 << plan.d >> 30} GiB >> 126 MB L2 (no flush needed)",
                    "value_def": "SURVEY 8(d) algorithmic bytes, 32 B x 2^d per ApplyFused leaf, / circuit time: "
                                 "an effective rate comparable with the reference arm; the bytes the sweeps "
-                                "actually move are in roofline.all_sweeps"},
+                                "actually move are in roofline.all_sweeps",
+                   "circuits_in_flight": in_flight(plan)},
         "circuit_ms": 1e3 * elapsed / args.steps,
         "gates_per_s": sum(len(t.payload["gates"]) for t in plan.tasks if t.kind == "ApplyFused")
                         * args.steps / elapsed,
