@@ -260,6 +260,7 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
         sparse = prog.sparse_start(dp, geo.D, unit) if (zero_start and SPARSE_START) else {}
         ld_xor = _fold_localize(dp, geo, sparse)
         st_keep = _prefix_store_masks(dp, geo, sparse)
+        out.st_keep = st_keep
         names, slots = jitmod.build_kernels(dp.buf, sparse=sparse, lazy=PIPELINED_JIT, ld_xor=ld_xor,
                                             st_keep=st_keep)
         out.zero_init = dict(jitmod._LAST_ZERO_INIT)
@@ -275,7 +276,15 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
         else:
             out.kernels = [jitmod.load_kernel(n, c, dev_index) for n, c in zip(names, slots)]
         out.jit_seconds = time.perf_counter() - t1
-    out.desc_bytes = [sum(prog.sparse_bytes(d, out.sparse.get(i))) for i, d in enumerate(dp.buf.descs)]
+    keep = getattr(out, "st_keep", {})
+
+    def launch_bytes(i, d):
+        rd, wr = prog.sparse_bytes(d, out.sparse.get(i))
+        if i in keep:  # a store mask writes one region of the masked bits
+            wr >>= bin(keep[i][0]).count("1")
+        return rd + wr
+
+    out.desc_bytes = [launch_bytes(i, d) for i, d in enumerate(dp.buf.descs)]
     _compile_cache.clear()  # keep one plan resident
     _compile_cache[key] = (plan, out)
     return out
