@@ -320,6 +320,19 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
             else:
                 w(f"    x[{v}] = tile[sb{si} ^ {offs[v]}u];")
 
+    # direct stores: the last stage's registers go straight to HBM when its
+    # lanes cover output bits 0-3 (every warp store writes whole 256-byte
+    # runs), skipping the shared-memory round trip of the store path.  Only
+    # for sweeps of two or more stages: a one-stage sweep is HBM-bound and
+    # its stores, spread over the next tile through shared memory, measured
+    # faster (QFT-30 sweep 3: 3.51 vs 3.57 ms; sweep 2, two stages: 0.97 -> 0.75)
+    tout = {sw.index(st_sw[i]): st_dev[i] for i in range(K)}
+    direct = False
+    if DIRECT_STORE and len(stage_info) >= 2 and K - rb >= 5:
+        regs_l, comp_l, _ = stage_info[-1]
+        direct = {0, 1, 2, 3} <= {tout[k] for k in comp_l[:5]}
+    if direct:
+        w(f"  const u64 dst_t = {_deposit('t', [tout[k] for k in comp_l])};")
     w("  double nrm = 0.0;")
     w(f"  long long tile_id = blockIdx.x;")
 
@@ -348,7 +361,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
         pf_chunks = chunks(NR)
     else:
         pf_chunks = [list(range(NR))] + [[] for _ in range(nslots - 1)]
-    st_chunks = chunks(NR)
+    st_chunks = [[] for _ in range(nslots)] if direct else chunks(NR)
 
     def prefetch_items(buf, base, items, commit=True):
         for it in items:
@@ -613,7 +626,22 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     flush()
     pending = []
 
-    if cur is not None:
+    if cur is not None and direct:
+        zm = zmask(cur)
+        for v in range(NR):
+            dev = sum(1 << tout[regs_l[q]] for q in range(rb) if (v >> q) & 1)
+            addr = f"state + chk(base | ((dst_t | {dev}ull) ^ {st_flip}ull))"
+            if v & zm:
+                val = "make_double2(0.0, 0.0)"
+            else:
+                val = f"x[{v}]"
+                w(f"    nrm = fma(x[{v}].x, x[{v}].x, fma(x[{v}].y, x[{v}].y, nrm));")
+            if st_keep is None:
+                w(f"    st_stream({addr}, {val});")
+            else:
+                km, kv = st_keep
+                w(f"    if (((dst_t ^ {dev ^ st_flip}ull) & {km}ull) == {kv}ull) st_stream({addr}, {val});")
+    elif cur is not None:
         store_regs(cur)
     if ahead:  # the next tile's slots, from loads issued at the start of this one
         nch = int(desc["lut_nch"])
@@ -627,7 +655,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     w("  }")
     # the last tile of this CTA is still in shared memory
     w("  __syncthreads();")
-    w("  if (iter > 0) {")
+    w(f"  if ({'false' if direct else 'iter > 0'}) {{")
     w(f"    double2* const pbuf = smem + ((iter - 1) % 3) * {TILE};")
     w("    const long long px = tile_id - gridDim.x;")
     w(f"    const u64 bp = {origin('px')};")
@@ -662,6 +690,8 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
 GROUP_OFFSET = os.environ.get("SVB200_JIT_GROUP_OFFSET", "1") not in ("0", "false", "no")
 GROUPS_ONLY = int(os.environ["SVB200_JIT_GROUPS_ONLY"]) if os.environ.get("SVB200_JIT_GROUPS_ONLY") else None
 SKIP_DEAD = os.environ.get("SVB200_JIT_SKIP_DEAD", "1") not in ("0", "false", "no")
+# the last stage stores straight from registers when that coalesces (kernel_source)
+DIRECT_STORE = os.environ.get("SVB200_JIT_DIRECT_STORE", "1") not in ("0", "false", "no")
 # sparse sweeps: known-zero registers drop out of the arithmetic (kernel_source)
 ZERO_TRACK = os.environ.get("SVB200_JIT_ZERO_TRACK", "1") not in ("0", "false", "no")
 # sweeps whose FP64 work per amplitude reaches this many DFMA (a fused 4x4 is

@@ -1340,14 +1340,20 @@ def emit_sweep(sp: SweepProgram, geo: DeviceGeometry, buf: ProgramBuffers, rb: i
     stages = _stages_sched(body, rb, tin) if STAGE_SCHED else _stages(body, rb)
     if not stages and (final.factors or sp.scale != 1):
         stages = [[set(), []]]
-    # pad register sets to exactly rb bits, preferring bits used soon after
+    # pad register sets to exactly rb bits, preferring bits used soon after;
+    # the last stage prefers bits that are not stored to output bits 0-4, so
+    # those stay on lanes and the stage can store straight from registers
+    # (jit.kernel_source direct stores)
+    low_out = {k for k in range(K) if sp.out_map[tin[k]][0] < 5}
     for si, st in enumerate(stages):
         need = st[0]
         for later in stages[si + 1:]:
             for b in sorted(later[0]):
                 if len(need) < rb and b not in need:
                     need.add(b)
-        for b in range(K):
+        last = si == len(stages) - 1 and len(stages) >= 2  # one-stage sweeps keep the smem store path
+        fill = sorted(range(K), key=lambda b: (b in low_out, b)) if last else range(K)
+        for b in fill:
             if len(need) >= rb:
                 break
             need.add(b)
