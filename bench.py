@@ -118,6 +118,8 @@ def fp64_all_sweeps(plan_, prof: dict, compute_s_per_step: float, steps: int):
         return None
     total = 0
     for di in range(len(comp.kernel_keys)):
+        if comp.kernel_keys[di] is None:  # merged into the sweep before it (no kernel)
+            continue
         cub = jitmod._cached(comp.kernel_keys[di])
         if cub is None:
             return None

@@ -155,6 +155,8 @@ SPARSE_START = os.environ.get("SVB200_SPARSE_START", "1") not in ("0", "false", 
 LOCALIZE = os.environ.get("SVB200_LOCALIZE", "1") not in ("0", "false", "no")
 # generated kernels compile in the background; each launch waits only for its own
 PIPELINED_JIT = os.environ.get("SVB200_JIT_PIPELINE", "1") not in ("0", "false", "no")
+# sparse sweeps that only expand dead bits are merged into the sweep before (_broadcast_merges)
+BROADCAST_MERGE = os.environ.get("SVB200_BROADCAST_MERGE", "1") not in ("0", "false", "no")
 # per-launch CUDA events around every sweep (bench.py's roofline); off by default
 PROFILE_SWEEPS = False
 # self-check mode (SVB200_GUARD_AMPS=n): guard bands of n amplitudes around the
@@ -200,6 +202,8 @@ class _Compiled:
     jit_seconds: float = 0.0
     zero_init: dict = field(default_factory=dict)  # descriptors that synthesise |0...0>
     sparse: dict = field(default_factory=dict)  # descriptor -> (support, full_out), prog.sparse_start
+    skip: set = field(default_factory=set)  # descriptors merged into the sweep before (_broadcast_merges)
+    bcast: dict = field(default_factory=dict)  # descriptor -> broadcast store (_broadcast_merges)
     n_sweeps: int = 0
 
 
@@ -261,8 +265,13 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
         ld_xor = _fold_localize(dp, geo, sparse)
         st_keep = _prefix_store_masks(dp, geo, sparse)
         out.st_keep = st_keep
+        bcast = _broadcast_merges(dp, geo, sparse, ld_xor, st_keep, overlap) if BROADCAST_MERGE else {}
+        out.skip = {j + 1 for j in bcast}
+        for j, (_, _, _, slot_j) in bcast.items():
+            descs[j]["norm_slot"] = slot_j
+        out.bcast = bcast
         names, slots = jitmod.build_kernels(dp.buf, sparse=sparse, lazy=PIPELINED_JIT, ld_xor=ld_xor,
-                                            st_keep=st_keep)
+                                            st_keep=st_keep, bcast=bcast, skip=out.skip)
         out.zero_init = dict(jitmod._LAST_ZERO_INIT)
         out.sparse = sparse
         for i, gcount in jitmod._LAST_GROUPS.items():  # launch geometry of two-group kernels
@@ -272,16 +281,22 @@ def compile_plan(plan, geo: prog.DeviceGeometry, device, jit=None, zero_start: b
         out.kernel_names = list(names)
         if PIPELINED_JIT:  # resolved at first launch (_kernel): early sweeps run while later ones compile
             out.kernels = list(slots)
-            out.kernel_keys = [sl.h for sl in slots]
+            out.kernel_keys = [sl.h if sl is not None else None for sl in slots]
         else:
-            out.kernels = [jitmod.load_kernel(n, c, dev_index) for n, c in zip(names, slots)]
+            out.kernels = [jitmod.load_kernel(n, c, dev_index) if n is not None else None
+                           for n, c in zip(names, slots)]
         out.jit_seconds = time.perf_counter() - t1
     keep = getattr(out, "st_keep", {})
+    bc = getattr(out, "bcast", {})
 
     def launch_bytes(i, d):
+        if i in out.skip:
+            return 0
         rd, wr = prog.sparse_bytes(d, out.sparse.get(i))
         if i in keep:  # a store mask writes one region of the masked bits
             wr >>= bin(keep[i][0]).count("1")
+        if i in bc:  # broadcast stores: every value to 2^|F| positions
+            wr <<= bin(bc[i][0]).count("1")
         return rd + wr
 
     out.desc_bytes = [launch_bytes(i, d) for i, d in enumerate(dp.buf.descs)]
@@ -667,7 +682,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             elif st.count:
                 _mark(f"sweeps{st.first}-{st.first + st.count - 1} start")
                 launched = _run_descs(compiled, st.first, st.count, state, rows_eff, L, norms, grid_limit,
-                                      stream)
+                                      stream, skip=compiled.skip)
                 _mark(f"sweeps{st.first}-{st.first + st.count - 1} end")
             elif slot in compiled.norm_alias:  # merged into a sweep of another leaf
                 pass
@@ -678,7 +693,7 @@ def run_plan(plan, shots: int | None = None, seed: int | None = None, initial=No
             else:
                 lib.svb_norm2(state.buf.data_ptr(), rows << L, norms[slot:].data_ptr(), stream)
                 launched = 1
-            stats.sweeps += st.count
+            stats.sweeps += st.count - sum(1 for di in range(st.first, st.first + st.count) if di in compiled.skip)
             stats.sweep_bytes += sum(compiled.desc_bytes[st.first:st.first + st.count])
             stats.kernel_launches += launched
             fused_order.append(task.id)
@@ -921,7 +936,8 @@ def _run_descs_overlapped(compiled, st, state, rows_eff, L, norms, grid_limit, s
         roles = compiled.overlap.get(di)
         if not roles:
             _mark(f"sweep{di} start")
-            launches += _run_descs(compiled, di, 1, state, rows_eff, L, norms, grid_limit, stream)
+            launches += _run_descs(compiled, di, 1, state, rows_eff, L, norms, grid_limit, stream,
+                                   skip=compiled.skip)
             _mark(f"sweep{di} end")
             continue
         group = roles["chain"].chain if "chain" in roles else [di]
@@ -1057,6 +1073,101 @@ def _alpha(st, geo: prog.DeviceGeometry) -> int:
     for ib, _ in st.swaps:
         alpha = (alpha << 1) | ((me >> (ib - geo.h)) & 1)
     return alpha
+
+
+def _broadcast_merges(dp, geo: prog.DeviceGeometry, sparse: dict, ld_xor: dict, st_keep: dict,
+                      overlap: dict) -> dict:
+    """Sparse sweeps whose only work is H on dead bits (plus constant
+    scales) merged into the sweep before them.
+
+    From |0...0>, a sweep j+1 whose every op is an H on a tile bit that is
+    still dead (all amplitudes with that bit set are zero) or a constant
+    scale just copies each amplitude v at position P (bits F clear) to the
+    2^|F| positions P | f, times the scale c: with x1 = 0 an H butterfly
+    (twiddles act on x1 only) gives x0 on both sides.  If its store keeps
+    every bit in place and it wakes every dead bit of its tile, sweep j can
+    write c * v to those positions directly and sweep j+1 is not launched
+    (QFT-30: the last sweep reads 4.3 GB and writes 17.2 GB to expand two
+    never-touched qubits).  Returns {j: (F mask, c, norm offset, norm slot
+    of j)}: the merged kernel adds sum |v|^2 at its norm slot when j ends a
+    leaf and 2^|F| sum |c v|^2 at slot + offset for j+1's leaf."""
+    out = {}
+    order = []  # launch order; None = a step between sweeps (remap, localize)
+    for st in dp.steps:
+        if st.kind in ("sweeps", "materialize"):
+            order.extend(range(st.first, st.first + st.count))
+        else:
+            order.append(None)
+    chunked = set(overlap) | {i for i, d in enumerate(dp.buf.descs) if d.get("cbits")}
+    for j, j1 in zip(order, order[1:]):
+        if j is None or j1 is None or j1 != j + 1 or j in out or (j - 1) in out:
+            continue
+        if j not in sparse or j1 not in sparse or sparse[j][1] or sparse[j][0] is None:
+            continue
+        if {j, j1} & (set(ld_xor) | set(st_keep) | chunked):
+            continue
+        m = _broadcast_only(dp, j1, sparse[j1], geo.D)
+        if m is None:
+            continue
+        fmask, c = m
+        slot_j, slot_1 = int(dp.buf.descs[j]["norm_slot"]), int(dp.buf.descs[j1]["norm_slot"])
+        if slot_j >= 0 and slot_1 >= 0:
+            out[j] = (fmask, c, slot_1 - slot_j, slot_j)
+        elif slot_1 >= 0:
+            out[j] = (fmask, c, 0, slot_1)
+        else:
+            out[j] = (fmask, c, None, slot_j)
+    return out
+
+
+def _broadcast_only(dp, i: int, sparse_i: tuple, D: int):
+    """(F mask of physical bits, scale) when sweep i only expands dead bits
+    (see _broadcast_merges), else None."""
+    supp, full_out = sparse_i
+    d = dp.buf.descs[i]
+    K = int(d["K"])
+    tin = [int(b) for b in d["tin"][:K]]
+    sw = [int(x) for x in d["sw"][:K]]
+    tout = {sw.index(int(d["st_sw"][q])): int(d["st_dev"][q]) for q in range(K)}
+    if int(d["st_flip"]) or any(tout[k] != tin[k] for k in range(K)) or d.get("cbits"):
+        return None
+    tinmask = sum(1 << b for b in tin)
+    if supp is None or (full_out and (supp | tinmask) != (1 << D) - 1):
+        return None  # it would also write zeros outside its live tiles
+    dead = tinmask & ~supp
+    ops = dp.buf.ops[d["op_begin"]: d["op_begin"] + d["op_count"]]
+    coef = dp.buf.coef
+    regs, woke, c, nconst = None, 0, complex(1.0), 0
+    for o in ops:
+        kind = int(o["kind"])
+        if kind == prog.OP_STAGE:
+            rm = int(o["rmask"])
+            regs = [k for k in range(K) if (rm >> k) & 1]
+            continue
+        if int(o["pmask"]) or regs is None:
+            return None
+        if kind == prog.OP_H:
+            if int(o["rmask"]):  # controlled
+                return None
+            b = tin[regs[int(o["a"])]]
+            if not (dead >> b) & 1 or (woke >> b) & 1:
+                return None
+            woke |= 1 << b
+        elif kind == prog.OP_SCALE:
+            c *= complex(coef[int(o["coef"])])
+            nconst += 1
+        elif kind == prog.OP_PHALL:
+            if int(o["ctab"]) >= 0 or int(o["tab"]) >= 0 or int(o["tf"]) >= 0:
+                return None
+            cp = complex(coef[int(o["coef"])])
+            c *= cp
+            nconst += cp != 1
+        else:
+            return None
+    # one constant multiply at most: the merged store then rounds exactly as the sweep would
+    if not woke or woke != dead or nconst > 1:
+        return None
+    return woke, c
 
 
 def _fold_localize(dp, geo: prog.DeviceGeometry, sparse: dict) -> dict:

@@ -162,8 +162,16 @@ def _warp_local_change(stage_info: list, a: int, b: int, nthreads: int) -> bool:
 
 
 def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int = 0,
-                  sparse: tuple | None = None, ld_xor: int = 0, st_keep: tuple | None = None) -> str:
+                  sparse: tuple | None = None, ld_xor: int = 0, st_keep: tuple | None = None,
+                  bcast: tuple | None = None) -> str:
     """Straight-line kernel for one sweep.
+
+    bcast = (F mask, c, norm offset, slot): every value v is stored as c * v
+    at its position P and at every P | f, f a combination of the F bits (the
+    next sweep only expanded those dead bits; executor._broadcast_merges).
+    Norms: sum |v|^2 at the launch's slot (offset None) or, for the merged
+    sweep's leaf, 2^|F| sum |c v|^2 at the slot + offset (only that one when
+    the offset is 0).
 
     st_keep = (mask, value): only positions whose tile bits at `mask` read
     `value` are stored (the last sweep of a replicated prefix: the localized
@@ -334,6 +342,8 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     if direct:
         w(f"  const u64 dst_t = {_deposit('t', [tout[k] for k in comp_l])};")
     w("  double nrm = 0.0;")
+    if bcast is not None and bcast[2] not in (None, 0):
+        w("  double nrm2 = 0.0;")
     w(f"  long long tile_id = blockIdx.x;")
 
     def origin(var):
@@ -384,6 +394,41 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
         if commit and items:
             w("      cp_async_commit();")
 
+    if bcast is not None:
+        bmask, bc, boff, _ = bcast
+        bbits = [b for b in range(D) if (bmask >> b) & 1]
+        bcombos = [sum(1 << bbits[i] for i in range(len(bbits)) if (m >> i) & 1) for m in range(1 << len(bbits))]
+
+    def emit_store(val, addr, pred=None, zero=False, ind="        "):
+        """One output value: norm terms, then its streaming store(s)."""
+        if bcast is None:
+            if not zero:
+                w(f"{ind}nrm = fma({val}.x, {val}.x, fma({val}.y, {val}.y, nrm));")
+            if pred is None:
+                w(f"{ind}st_stream(state + chk({addr}), {val});")
+            else:
+                w(f"{ind}if ({pred})")
+                w(f"{ind}  st_stream(state + chk({addr}), {val});")
+            return
+        else:
+            if zero:
+                cv = "make_double2(0.0, 0.0)"
+            else:
+                w(f"        const double2 cv_ = {_cmul_lit(val, bc)};")
+                cv = "cv_"
+                if boff is None or boff != 0:
+                    w(f"        nrm = fma(({val}).x, ({val}).x, fma(({val}).y, ({val}).y, nrm));")
+                if boff is not None:
+                    acc = "nrm" if boff == 0 else "nrm2"
+                    w(f"        {acc} = fma(cv_.x, cv_.x, fma(cv_.y, cv_.y, {acc}));")
+            stores = [(f"state + chk(({addr}) | {f}ull)", cv) for f in bcombos]
+        if pred is not None:
+            w(f"        if ({pred}) {{")
+        for a, v in stores:
+            w(f"        st_stream({a}, {v});")
+        if pred is not None:
+            w("        }")
+
     def store_items(buf, base, items):
         for it in items:
             dev = 0
@@ -394,13 +439,11 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                     s ^= st_sw[tb + q]
             w("      {")
             w(f"        const double2 v = {buf}[sts_t ^ {s}u];")
-            w("        nrm = fma(v.x, v.x, fma(v.y, v.y, nrm));")
-            if st_keep is None:
-                w(f"        st_stream(state + chk({base} | ((st_t | {dev}ull) ^ {st_flip}ull)), v);")
-            else:
+            pred = None
+            if st_keep is not None:
                 km, kv = st_keep
-                w(f"        if (((st_t ^ {dev ^ st_flip}ull) & {km}ull) == {kv}ull)")
-                w(f"          st_stream(state + chk({base} | ((st_t | {dev}ull) ^ {st_flip}ull)), v);")
+                pred = f"((st_t ^ {dev ^ st_flip}ull) & {km}ull) == {kv}ull"
+            emit_store("v", f"{base} | ((st_t | {dev}ull) ^ {st_flip}ull)", pred)
             w("      }")
 
     def slot(j):
@@ -630,17 +673,14 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
         zm = zmask(cur)
         for v in range(NR):
             dev = sum(1 << tout[regs_l[q]] for q in range(rb) if (v >> q) & 1)
-            addr = f"state + chk(base | ((dst_t | {dev}ull) ^ {st_flip}ull))"
-            if v & zm:
-                val = "make_double2(0.0, 0.0)"
-            else:
-                val = f"x[{v}]"
-                w(f"    nrm = fma(x[{v}].x, x[{v}].x, fma(x[{v}].y, x[{v}].y, nrm));")
-            if st_keep is None:
-                w(f"    st_stream({addr}, {val});")
-            else:
+            pred = None
+            if st_keep is not None:
                 km, kv = st_keep
-                w(f"    if (((dst_t ^ {dev ^ st_flip}ull) & {km}ull) == {kv}ull) st_stream({addr}, {val});")
+                pred = f"((dst_t ^ {dev ^ st_flip}ull) & {km}ull) == {kv}ull"
+            w("    {")
+            emit_store("make_double2(0.0, 0.0)" if v & zm else f"x[{v}]",
+                       f"base | ((dst_t | {dev}ull) ^ {st_flip}ull)", pred, zero=bool(v & zm), ind="      ")
+            w("    }")
     elif cur is not None:
         store_regs(cur)
     if ahead:  # the next tile's slots, from loads issued at the start of this one
@@ -672,16 +712,21 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
         w("  }")
     w("  if (norm_out != nullptr) {")
     full = "0xffffffffu" if NT >= 32 else f"{(1 << NT) - 1}u"
-    for o in (16, 8, 4, 2, 1):
-        if o < NT:
-            w(f"    nrm += __shfl_xor_sync({full}, nrm, {o});")
-    w("    if ((t & 31) == 0) red[t >> 5] = nrm;")
-    w("    __syncthreads();")
-    w("    if (t == 0) {")
-    w("      double s = 0.0;")
-    w(f"      for (int i = 0; i < {(NT + 31) // 32}; ++i) s += red[i];")
-    w("      atomicAdd(norm_out, s);")
-    w("    }")
+    two = bcast is not None and bcast[2] not in (None, 0)
+    for acc, dst, mult in ([("nrm", "norm_out", len(bcombos) if bcast is not None and bcast[2] == 0 else 1)]
+                           + ([("nrm2", f"norm_out + {bcast[2]}", len(bcombos))] if two else [])):
+        for o in (16, 8, 4, 2, 1):
+            if o < NT:
+                w(f"    {acc} += __shfl_xor_sync({full}, {acc}, {o});")
+        w(f"    if ((t & 31) == 0) red[t >> 5] = {acc};")
+        w("    __syncthreads();")
+        w("    if (t == 0) {")
+        w("      double s = 0.0;")
+        w(f"      for (int i = 0; i < {(NT + 31) // 32}; ++i) s += red[i];")
+        w(f"      atomicAdd({dst}, {_lit_raw(float(mult))} * s);" if mult != 1 else f"      atomicAdd({dst}, s);")
+        w("    }")
+        if two and acc == "nrm":  # red[] is reused for the second sum
+            w("    __syncthreads();")
     w("  }")
     w("}")
     return "\n".join(_pool_end(L)) + "\n"
@@ -1304,8 +1349,12 @@ def _nvrtc(src: str, name: str, h: str) -> bytes:
 
 def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: int | None = None,
                   zero_init: dict | None = None, sparse: dict | None = None, lazy: bool = False,
-                  ld_xor: dict | None = None, st_keep: dict | None = None):
+                  ld_xor: dict | None = None, st_keep: dict | None = None, bcast: dict | None = None,
+                  skip=()):
     """Generate + compile one kernel per sweep descriptor; returns (names, cubins).
+
+    bcast: descriptor -> broadcast store (executor._broadcast_merges); skip:
+    descriptors merged into the sweep before them (no kernel, name None).
 
     zero_init maps descriptor index -> 1/2 for sweeps whose input is known to
     be |0...0> (see kernel_source); _LAST_ZERO_INIT records which were used.
@@ -1320,7 +1369,11 @@ def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: in
             zero_init[i] = 2 if supp is None else 1
     used = {}
     groups = {}
+    bcast = dict(bcast or {})
     for i, d in enumerate(buf.descs):
+        if i in skip:
+            names.append(None)
+            continue
         ops = buf.ops[d["op_begin"]: d["op_begin"] + d["op_count"]]
         zi = zero_init.get(i, 0)
         if zi and not (zi == 2 and i in sparse) and not any(int(o["kind"]) == prog.OP_STAGE for o in ops):
@@ -1334,11 +1387,11 @@ def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: in
         gen = kernel_source_2g if two else kernel_source
         if two:
             groups[i] = 2
-        if (ld_xor or {}).get(i) or (st_keep or {}).get(i):
-            gen = kernel_source  # the one-group kernel carries the load XOR / store mask
+        if (ld_xor or {}).get(i) or (st_keep or {}).get(i) or i in bcast:
+            gen = kernel_source  # the one-group kernel carries the load XOR / store mask / broadcast
             groups.pop(i, None)
             body = gen("KNAME", d, ops, buf.coef, zi, sparse.get(i), (ld_xor or {}).get(i, 0),
-                       (st_keep or {}).get(i))
+                       (st_keep or {}).get(i), bcast.get(i))
         else:
             body = gen("KNAME", d, ops, buf.coef, zi, sparse.get(i))
         h = hashlib.sha1(body.encode()).hexdigest()[:16]
@@ -1349,10 +1402,11 @@ def build_kernels(buf: prog.ProgramBuffers, prefix: str = "svb_jit", threads: in
     _LAST_ZERO_INIT.update(used)
     _LAST_GROUPS.clear()
     _LAST_GROUPS.update(groups)
-    slots = compile_async(srcs, names, threads)
+    built = iter(compile_async(srcs, [n for n in names if n is not None], threads))
+    slots = [None if n is None else next(built) for n in names]
     if lazy:
         return names, slots
-    return names, [sl.cubin() for sl in slots]
+    return names, [None if sl is None else sl.cubin() for sl in slots]
 
 
 class KernelSlot:

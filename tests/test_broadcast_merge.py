@@ -1,0 +1,90 @@
+"""Broadcast merge (executor._broadcast_merges): a sparse sweep that only
+expands never-touched qubits (H on dead bits, one constant scale) is folded
+into the store of the sweep before it."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+PLANS = Path(__file__).resolve().parent.parent / "plans"
+
+
+def load(name):
+    from paper_2509_14098_b200 import plan as planmod
+
+    return planmod.load(str(PLANS / f"{name}.json.gz"))
+
+
+def merges(name):
+    from paper_2509_14098_b200 import executor as ex, program as prog
+
+    plan = load(name)
+    geo = prog.DeviceGeometry(d=plan.d, g=plan.g, h=plan.g, rank_base=0, pad_to=prog.RB)
+    dp = prog.plan_device(plan, geo, rb=4, overlap_bits=0, free_start=True, stable_threads=False)
+    sparse = prog.sparse_start(dp, geo.D, True)
+    return dp, sparse, ex._broadcast_merges(dp, geo, sparse, {}, {}, {})
+
+
+def test_qft30_last_sweep_is_a_broadcast_of_two_qubits():
+    """QFT-30's last sweep only applies H to qubits 28 and 29, which no
+    earlier gate touched: it merges into sweep 2 with F = {28, 29} and the
+    scale of the two H gates; sweep 2 keeps its own leaf norm and adds the
+    merged leaf's at the other slot."""
+    dp, sparse, bc = merges("qft30_h30-12")
+    assert set(bc) == {2}
+    fmask, c, off, slot = bc[2]
+    assert fmask == (1 << 28) | (1 << 29)
+    assert abs(c - 0.5) < 1e-15
+    assert slot == int(dp.buf.descs[2]["norm_slot"]) and off == int(dp.buf.descs[3]["norm_slot"]) - slot
+    # the merged sweep wrote only the support; the broadcast covers the rest
+    supp, full_out = sparse[3]
+    assert full_out and supp | fmask == (1 << 30) - 1
+
+
+def test_no_merge_when_the_sweep_computes():
+    """QV and a sweep that mixes live amplitudes never merge."""
+    _, _, bc = merges("qv30_h30-12")
+    assert bc == {}
+
+
+def test_merge_source_stores_every_combination():
+    from paper_2509_14098_b200 import jit
+
+    dp, sparse, bc = merges("qft22_h22-12")
+    (j, (fmask, c, off, slot)), = bc.items()
+    d = dp.buf.descs[j]
+    ops = dp.buf.ops[d["op_begin"]: d["op_begin"] + d["op_count"]]
+    src = jit.kernel_source("k", d, ops, dp.buf.coef, 0, sparse[j], 0, None, bc[j])
+    nf = bin(fmask).count("1")
+    stores = src.count("st_stream(")
+    plain = jit.kernel_source("k", d, ops, dp.buf.coef, 0, sparse[j]).count("st_stream(")
+    assert stores == plain * (1 << nf)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["qft22_h22-12", "qft28_h28-12", "qft30_h30-12"])
+def test_merged_equals_unmerged_and_closed_form(name):
+    """Merged and unmerged runs give equal amplitudes and norms, and QFT|0>
+    is the uniform state 2^-d/2 (every broadcast position written)."""
+    import torch
+
+    from paper_2509_14098_b200 import executor, run_plan
+
+    plan = load(name)
+    a = run_plan(plan)
+    sa = a.stats.sweeps
+    blocks_a = a.state.blocks
+    executor.BROADCAST_MERGE = False
+    executor._compile_cache.clear()
+    try:
+        b = run_plan(plan)
+        assert torch.equal(blocks_a, b.state.blocks), name
+        assert b.stats.sweeps == sa + 1
+    finally:
+        executor.BROADCAST_MERGE = True
+        executor._compile_cache.clear()
+    u = 2.0 ** (-plan.d / 2)
+    err = (blocks_a - u).abs().max().item()
+    assert err < 1e-12, (name, err)
+    assert np.isfinite(err)

@@ -100,7 +100,9 @@ def test_qft30_bench_plan_closed_form():
     assert _closed_form_err(res.state, x) < 1e-10
     del res
     res = run_plan(plan)  # |0...0>: sparse support-only sweeps
-    assert res.stats.sweeps == 4
+    # the fourth sweep only expands qubits 28-29 and is merged into the
+    # third's stores (executor._broadcast_merges)
+    assert res.stats.sweeps == 3
     assert _closed_form_err(res.state, 0) < 1e-12
 
 
