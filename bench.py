@@ -48,7 +48,7 @@ UNIT = "GB/s"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 E2E_HOST_BYTES = 48 << 30  # pinned host buffers per process (in and out each)
-TRAFFIC_REV = "r02b"  # profiles/traffic.json entries measured on the current sweep code
+TRAFFIC_REV = "r02c"  # profiles/traffic.json entries measured on the current sweep code
 E2E_PIPELINE = os.environ.get("SVB200_E2E_PIPELINE", "1") != "0"  # two circuits in flight
 PIPELINE = os.environ.get("SVB200_BENCH_PIPELINE", "1") != "0"  # timed loop: two circuits in flight when they fit
 

@@ -669,7 +669,25 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     flush()
     pending = []
 
-    if cur is not None and direct:
+    if cur is not None and direct and bcast is not None and BCAST_F_OUTER and st_keep is None:
+        # broadcast copies grouped by region: all values of one f, then the next
+        zm = zmask(cur)
+        bm, bc, boff, _ = bcast
+        for v in range(NR):
+            if v & zm:
+                continue
+            if boff is None or boff != 0:
+                w(f"    nrm = fma(x[{v}].x, x[{v}].x, fma(x[{v}].y, x[{v}].y, nrm));")
+            w(f"    x[{v}] = {_cmul_lit(f'x[{v}]', bc)};")
+            if boff is not None:
+                acc = "nrm" if boff == 0 else "nrm2"
+                w(f"    {acc} = fma(x[{v}].x, x[{v}].x, fma(x[{v}].y, x[{v}].y, {acc}));")
+        for f in bcombos:
+            for v in range(NR):
+                dev = sum(1 << tout[regs_l[q]] for q in range(rb) if (v >> q) & 1)
+                val = "make_double2(0.0, 0.0)" if v & zm else f"x[{v}]"
+                w(f"    st_stream(state + chk((base | ((dst_t | {dev}ull) ^ {st_flip}ull)) | {f}ull), {val});")
+    elif cur is not None and direct:
         zm = zmask(cur)
         for v in range(NR):
             dev = sum(1 << tout[regs_l[q]] for q in range(rb) if (v >> q) & 1)
@@ -737,6 +755,7 @@ GROUPS_ONLY = int(os.environ["SVB200_JIT_GROUPS_ONLY"]) if os.environ.get("SVB20
 SKIP_DEAD = os.environ.get("SVB200_JIT_SKIP_DEAD", "1") not in ("0", "false", "no")
 # the last stage stores straight from registers when that coalesces (kernel_source)
 DIRECT_STORE = os.environ.get("SVB200_JIT_DIRECT_STORE", "1") not in ("0", "false", "no")
+BCAST_F_OUTER = os.environ.get("SVB200_JIT_BCAST_F_OUTER", "0") not in ("0", "false", "no")
 # sparse sweeps: known-zero registers drop out of the arithmetic (kernel_source)
 ZERO_TRACK = os.environ.get("SVB200_JIT_ZERO_TRACK", "1") not in ("0", "false", "no")
 # sweeps whose FP64 work per amplitude reaches this many DFMA (a fused 4x4 is
