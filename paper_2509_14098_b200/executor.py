@@ -1092,11 +1092,11 @@ def _broadcast_merges(dp, geo: prog.DeviceGeometry, sparse: dict, ld_xor: dict, 
     of j)}: the merged kernel adds sum |v|^2 at its norm slot when j ends a
     leaf and 2^|F| sum |c v|^2 at slot + offset for j+1's leaf."""
     out = {}
-    order = []  # launch order; None = a step between sweeps (remap, localize)
+    order = []  # launch order; None = a step between sweeps (remap, unfolded localize)
     for st in dp.steps:
         if st.kind in ("sweeps", "materialize"):
             order.extend(range(st.first, st.first + st.count))
-        else:
+        elif not (st.kind == "localize" and st.folded):  # a folded localize moves nothing
             order.append(None)
     chunked = set(overlap) | {i for i, d in enumerate(dp.buf.descs) if d.get("cbits")}
     for j, j1 in zip(order, order[1:]):
@@ -1104,12 +1104,20 @@ def _broadcast_merges(dp, geo: prog.DeviceGeometry, sparse: dict, ld_xor: dict, 
             continue
         if j not in sparse or j1 not in sparse or sparse[j][1] or sparse[j][0] is None:
             continue
-        if {j, j1} & (set(ld_xor) | set(st_keep) | chunked):
+        if {j, j1} & chunked or j in ld_xor or j1 in st_keep:
             continue
         m = _broadcast_only(dp, j1, sparse[j1], geo.D)
         if m is None:
             continue
-        fmask, c = m
+        fmask, c = m  # c: combination -> constants
+        # across a folded localized remap: sweep j keeps region alpha of the
+        # swapped bits and sweep j+1 reads it through a load XOR; when the
+        # broadcast covers those bits, storing each kept value at every
+        # combination of them (the region bits cleared) is the same
+        if j in st_keep and st_keep[j][0] & ~fmask:
+            continue
+        if j1 in ld_xor and ld_xor[j1] & ~fmask:
+            continue
         slot_j, slot_1 = int(dp.buf.descs[j]["norm_slot"]), int(dp.buf.descs[j1]["norm_slot"])
         if slot_j >= 0 and slot_1 >= 0:
             out[j] = (fmask, c, slot_1 - slot_j, slot_j)
@@ -1121,15 +1129,24 @@ def _broadcast_merges(dp, geo: prog.DeviceGeometry, sparse: dict, ld_xor: dict, 
 
 
 def _broadcast_only(dp, i: int, sparse_i: tuple, D: int):
-    """(F mask of physical bits, scale) when sweep i only expands dead bits
-    (see _broadcast_merges), else None."""
+    """(F mask, {f: constants}) when sweep i only expands dead bits (see
+    _broadcast_merges), else None.
+
+    The op list is replayed on the one nonzero input of each group (x0,
+    every dead-bit combination zero): an H (fused or not; twiddles act on
+    the zero half) copies x0 to both sides, a 2x2 / 4x4 on dead bits sends
+    x0 times its first column to the combinations, an X moves it, a phase
+    anchored on a dead bit touches only zeros, and scales multiply every
+    copy.  Each combination f keeps the constants in the order the sweep
+    would multiply them (the merged store repeats them, so the values are
+    bit-identical); a combination missing from the map is zero."""
     supp, full_out = sparse_i
     d = dp.buf.descs[i]
     K = int(d["K"])
     tin = [int(b) for b in d["tin"][:K]]
     sw = [int(x) for x in d["sw"][:K]]
     tout = {sw.index(int(d["st_sw"][q])): int(d["st_dev"][q]) for q in range(K)}
-    if int(d["st_flip"]) or any(tout[k] != tin[k] for k in range(K)) or d.get("cbits"):
+    if int(d["st_flip"]) or d.get("cbits"):
         return None
     tinmask = sum(1 << b for b in tin)
     if supp is None or (full_out and (supp | tinmask) != (1 << D) - 1):
@@ -1137,7 +1154,13 @@ def _broadcast_only(dp, i: int, sparse_i: tuple, D: int):
     dead = tinmask & ~supp
     ops = dp.buf.ops[d["op_begin"]: d["op_begin"] + d["op_count"]]
     coef = dp.buf.coef
-    regs, woke, c, nconst = None, 0, complex(1.0), 0
+    regs, woke = None, 0
+    copies = {0: []}  # combination of woken bits -> constants applied to x0
+
+    def fresh(slot):
+        b = tin[regs[slot]]
+        return b if (dead >> b) & 1 and not (woke >> b) & 1 else None
+
     for o in ops:
         kind = int(o["kind"])
         if kind == prog.OP_STAGE:
@@ -1146,28 +1169,66 @@ def _broadcast_only(dp, i: int, sparse_i: tuple, D: int):
             continue
         if int(o["pmask"]) or regs is None:
             return None
-        if kind == prog.OP_H:
-            if int(o["rmask"]):  # controlled
+        if kind in (prog.OP_H, prog.OP_U1, prog.OP_X):
+            b = fresh(int(o["a"]))
+            if int(o["rmask"]) or b is None:  # controlled, or on a live bit: real mixing
                 return None
-            b = tin[regs[int(o["a"])]]
-            if not (dead >> b) & 1 or (woke >> b) & 1:
+            bit = 1 << b
+            if kind == prog.OP_H:
+                copies = {**copies, **{f | bit: list(ch) for f, ch in copies.items()}}
+            elif kind == prog.OP_X:
+                copies = {f | bit: ch for f, ch in copies.items()}
+            else:
+                m00, m10 = complex(coef[int(o["coef"])]), complex(coef[int(o["coef"]) + 2])
+                nxt = {}
+                for f, ch in copies.items():
+                    if m00 != 0:
+                        nxt[f] = ch + [m00]
+                    if m10 != 0:
+                        nxt[f | bit] = ch + [m10]
+                copies = nxt
+            woke |= bit
+        elif kind == prog.OP_U2:
+            ba, bb = fresh(int(o["a"])), fresh(int(o["b"]))
+            if ba is None or bb is None:
                 return None
-            woke |= 1 << b
+            M = np.asarray(coef[int(o["coef"]): int(o["coef"]) + 16]).reshape(4, 4)
+            nxt = {}
+            for f, ch in copies.items():
+                for r in range(4):  # rows in _emit_op order: (b, a) = (r & 1, r >> 1)
+                    if M[r, 0] != 0:
+                        nxt[f | ((r & 1) << bb) | ((r >> 1) << ba)] = ch + [complex(M[r, 0])]
+            copies = nxt
+            woke |= (1 << ba) | (1 << bb)
+        elif kind == prog.OP_PH:
+            if fresh(int(o["a"])) is None:  # a phase on amplitudes that can be nonzero
+                return None
         elif kind == prog.OP_SCALE:
-            c *= complex(coef[int(o["coef"])])
-            nconst += 1
+            cs = complex(coef[int(o["coef"])])
+            copies = {f: ch + [cs] for f, ch in copies.items()}
         elif kind == prog.OP_PHALL:
             if int(o["ctab"]) >= 0 or int(o["tab"]) >= 0 or int(o["tf"]) >= 0:
                 return None
             cp = complex(coef[int(o["coef"])])
-            c *= cp
-            nconst += cp != 1
+            if cp != 1:
+                copies = {f: ch + [cp] for f, ch in copies.items()}
         else:
             return None
-    # one constant multiply at most: the merged store then rounds exactly as the sweep would
-    if not woke or woke != dead or nconst > 1:
+    if not woke or woke != dead:
         return None
-    return woke, c
+    # the store may permute the woken bits among themselves (a final relabel);
+    # every other bit must stay in place
+    for k in range(K):
+        if (woke >> tin[k]) & 1:
+            if not (woke >> tout[k]) & 1:
+                return None
+        elif tout[k] != tin[k]:
+            return None
+    out_bit = {tin[k]: tout[k] for k in range(K)}
+    moved = {}
+    for f, ch in copies.items():
+        moved[sum(1 << out_bit[b] for b in range(D) if (f >> b) & 1)] = ch
+    return woke, moved
 
 
 def _fold_localize(dp, geo: prog.DeviceGeometry, sparse: dict) -> dict:

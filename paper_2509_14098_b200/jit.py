@@ -395,12 +395,14 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
             w("      cp_async_commit();")
 
     if bcast is not None:
-        bmask, bc, boff, _ = bcast
+        bmask, bchains, boff, _ = bcast
         bbits = [b for b in range(D) if (bmask >> b) & 1]
         bcombos = [sum(1 << bbits[i] for i in range(len(bbits)) if (m >> i) & 1) for m in range(1 << len(bbits))]
 
     def emit_store(val, addr, pred=None, zero=False, ind="        "):
-        """One output value: norm terms, then its streaming store(s)."""
+        """One output value: norm terms, then its streaming store(s).  With
+        bcast, the copy at combination f is v times f's constants in the
+        order the merged sweep would multiply them (bit-identical values)."""
         if bcast is None:
             if not zero:
                 w(f"{ind}nrm = fma({val}.x, {val}.x, fma({val}.y, {val}.y, nrm));")
@@ -410,22 +412,31 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                 w(f"{ind}if ({pred})")
                 w(f"{ind}  st_stream(state + chk({addr}), {val});")
             return
-        else:
-            if zero:
-                cv = "make_double2(0.0, 0.0)"
-            else:
-                w(f"        const double2 cv_ = {_cmul_lit(val, bc)};")
-                cv = "cv_"
-                if boff is None or boff != 0:
-                    w(f"        nrm = fma(({val}).x, ({val}).x, fma(({val}).y, ({val}).y, nrm));")
-                if boff is not None:
-                    acc = "nrm" if boff == 0 else "nrm2"
-                    w(f"        {acc} = fma(cv_.x, cv_.x, fma(cv_.y, cv_.y, {acc}));")
-            stores = [(f"state + chk(({addr}) | {f}ull)", cv) for f in bcombos]
+        names = {}
+        copies = []
+        for f in bcombos:
+            ch = bchains.get(f)
+            if zero or ch is None:
+                copies.append((f, "make_double2(0.0, 0.0)", False))
+                continue
+            key = tuple(ch)
+            if key not in names:
+                e = val
+                for c in ch:
+                    e = _cmul_lit(e, c)
+                names[key] = f"cv{len(names)}_"
+                w(f"        const double2 {names[key]} = {e};")
+            copies.append((f, names[key], True))
+        if not zero and (boff is None or boff != 0):  # this sweep's own leaf: every value
+            w(f"        nrm = fma(({val}).x, ({val}).x, fma(({val}).y, ({val}).y, nrm));")
         if pred is not None:
             w(f"        if ({pred}) {{")
-        for a, v in stores:
-            w(f"        st_stream({a}, {v});")
+        for f, cv, live in copies:
+            if live and boff is not None:  # the merged leaf: the values stored
+                acc = "nrm" if boff == 0 else "nrm2"
+                w(f"        {acc} = fma({cv}.x, {cv}.x, fma({cv}.y, {cv}.y, {acc}));")
+            # the positions' F bits are cleared first: a kept region (st_keep) may set them
+            w(f"        st_stream(state + chk((({addr}) & {~bmask & ((1 << 64) - 1)}ull) | {f}ull), {cv});")
         if pred is not None:
             w("        }")
 
@@ -669,25 +680,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     flush()
     pending = []
 
-    if cur is not None and direct and bcast is not None and BCAST_F_OUTER and st_keep is None:
-        # broadcast copies grouped by region: all values of one f, then the next
-        zm = zmask(cur)
-        bm, bc, boff, _ = bcast
-        for v in range(NR):
-            if v & zm:
-                continue
-            if boff is None or boff != 0:
-                w(f"    nrm = fma(x[{v}].x, x[{v}].x, fma(x[{v}].y, x[{v}].y, nrm));")
-            w(f"    x[{v}] = {_cmul_lit(f'x[{v}]', bc)};")
-            if boff is not None:
-                acc = "nrm" if boff == 0 else "nrm2"
-                w(f"    {acc} = fma(x[{v}].x, x[{v}].x, fma(x[{v}].y, x[{v}].y, {acc}));")
-        for f in bcombos:
-            for v in range(NR):
-                dev = sum(1 << tout[regs_l[q]] for q in range(rb) if (v >> q) & 1)
-                val = "make_double2(0.0, 0.0)" if v & zm else f"x[{v}]"
-                w(f"    st_stream(state + chk((base | ((dst_t | {dev}ull) ^ {st_flip}ull)) | {f}ull), {val});")
-    elif cur is not None and direct:
+    if cur is not None and direct:
         zm = zmask(cur)
         for v in range(NR):
             dev = sum(1 << tout[regs_l[q]] for q in range(rb) if (v >> q) & 1)
@@ -731,8 +724,7 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     w("  if (norm_out != nullptr) {")
     full = "0xffffffffu" if NT >= 32 else f"{(1 << NT) - 1}u"
     two = bcast is not None and bcast[2] not in (None, 0)
-    for acc, dst, mult in ([("nrm", "norm_out", len(bcombos) if bcast is not None and bcast[2] == 0 else 1)]
-                           + ([("nrm2", f"norm_out + {bcast[2]}", len(bcombos))] if two else [])):
+    for acc, dst, mult in [("nrm", "norm_out", 1)] + ([("nrm2", f"norm_out + {bcast[2]}", 1)] if two else []):
         for o in (16, 8, 4, 2, 1):
             if o < NT:
                 w(f"    {acc} += __shfl_xor_sync({full}, {acc}, {o});")
@@ -755,7 +747,6 @@ GROUPS_ONLY = int(os.environ["SVB200_JIT_GROUPS_ONLY"]) if os.environ.get("SVB20
 SKIP_DEAD = os.environ.get("SVB200_JIT_SKIP_DEAD", "1") not in ("0", "false", "no")
 # the last stage stores straight from registers when that coalesces (kernel_source)
 DIRECT_STORE = os.environ.get("SVB200_JIT_DIRECT_STORE", "1") not in ("0", "false", "no")
-BCAST_F_OUTER = os.environ.get("SVB200_JIT_BCAST_F_OUTER", "0") not in ("0", "false", "no")
 # sparse sweeps: known-zero registers drop out of the arithmetic (kernel_source)
 ZERO_TRACK = os.environ.get("SVB200_JIT_ZERO_TRACK", "1") not in ("0", "false", "no")
 # sweeps whose FP64 work per amplitude reaches this many DFMA (a fused 4x4 is

@@ -33,9 +33,10 @@ def test_qft30_last_sweep_is_a_broadcast_of_two_qubits():
     merged leaf's at the other slot."""
     dp, sparse, bc = merges("qft30_h30-12")
     assert set(bc) == {2}
-    fmask, c, off, slot = bc[2]
+    fmask, copies, off, slot = bc[2]
     assert fmask == (1 << 28) | (1 << 29)
-    assert abs(c - 0.5) < 1e-15
+    assert sorted(copies) == [0, 1 << 28, 1 << 29, 3 << 28]
+    assert all(len(ch) == 1 and abs(ch[0] - 0.5) < 1e-15 for ch in copies.values())
     assert slot == int(dp.buf.descs[2]["norm_slot"]) and off == int(dp.buf.descs[3]["norm_slot"]) - slot
     # the merged sweep wrote only the support; the broadcast covers the rest
     supp, full_out = sparse[3]
@@ -52,7 +53,7 @@ def test_merge_source_stores_every_combination():
     from paper_2509_14098_b200 import jit
 
     dp, sparse, bc = merges("qft22_h22-12")
-    (j, (fmask, c, off, slot)), = bc.items()
+    (j, (fmask, copies, off, slot)), = bc.items()
     d = dp.buf.descs[j]
     ops = dp.buf.ops[d["op_begin"]: d["op_begin"] + d["op_count"]]
     src = jit.kernel_source("k", d, ops, dp.buf.coef, 0, sparse[j], 0, None, bc[j])
@@ -60,6 +61,34 @@ def test_merge_source_stores_every_combination():
     stores = src.count("st_stream(")
     plain = jit.kernel_source("k", d, ops, dp.buf.coef, 0, sparse[j]).count("st_stream(")
     assert stores == plain * (1 << nf)
+
+
+def test_multi_gpu_merges_cross_the_folded_localize():
+    """On 2 and 4 GPUs the last prefix sweep keeps region alpha and the
+    sweep after the folded localized remap only expands the swapped bits
+    (on 4 GPUs a fused 4x4 on them, with the final relabel of the two bits):
+    both merge, for every rank."""
+    from paper_2509_14098_b200 import executor as ex, program as prog
+
+    for name, world in (("qft31_h30-12", 2), ("qft32_h30-12", 4)):
+        plan = load(name)
+        rows = (1 << plan.g) // world
+        for me in range(world):
+            geo = prog.DeviceGeometry(d=plan.d, g=plan.g, h=rows.bit_length() - 1, rank_base=me * rows,
+                                      pad_to=prog.RB)
+            dp0 = prog.plan_device(plan, geo, rb=4, overlap_bits=0, free_start=True, stable_threads=False)
+            rep = prog.localize_applies(dp0, geo.D, world, geo.h)
+            assert rep
+            dp = prog.plan_device(plan, geo, rb=4, overlap_bits=0, free_start=True, stable_threads=False,
+                                  overlap_skip_first=True, replicate_prefix=True)
+            sparse = prog.sparse_start(dp, geo.D, True)
+            ldx = ex._fold_localize(dp, geo, sparse)
+            stk = ex._prefix_store_masks(dp, geo, sparse)
+            bc = ex._broadcast_merges(dp, geo, sparse, ldx, stk, {})
+            assert len(bc) == 1, (name, me)
+            (j, (fmask, copies, off, slot)), = bc.items()
+            assert bin(fmask).count("1") == world.bit_length() - 1
+            assert len(copies) == world
 
 
 @pytest.mark.gpu
