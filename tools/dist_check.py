@@ -105,12 +105,12 @@ def scale_checks(me, world):
         plan = planmod.load(str(ROOT / "plans" / f"{name}.json.gz"))
         if (1 << plan.g) < world:
             continue
-        if plan.d - plan.g >= 32 or "--colocate" in sys.argv:
-            # 64+ GiB per GPU, or every process on one GPU: return the pooled buffers of earlier runs first
-            from paper_2509_14098_b200 import comm
+        # return the pooled buffers of earlier runs first (a 128 GiB QFT-34
+        # arena and the mirrors' own would not fit together)
+        from paper_2509_14098_b200 import comm
 
-            comm.release_arenas()
-            torch.cuda.empty_cache()
+        comm.release_arenas()
+        torch.cuda.empty_cache()
         res = run_plan(plan)
         flat = res.state.blocks.reshape(-1)
         err = torch.zeros(1, dtype=torch.float64, device=flat.device)
