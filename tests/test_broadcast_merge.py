@@ -117,3 +117,21 @@ def test_merged_equals_unmerged_and_closed_form(name):
     err = (blocks_a - u).abs().max().item()
     assert err < 1e-12, (name, err)
     assert np.isfinite(err)
+
+
+@pytest.mark.gpu
+def test_merged_plan_against_the_oracle():
+    """QFT-22 from |0...0> (its last sweep merges) against the CPU
+    restatement of the reference executor, every amplitude."""
+    import os
+
+    from oracle import oracle as orc
+    from paper_2509_14098_b200 import run_plan
+
+    plan = load("qft22_h22-12")
+    res = run_plan(plan)
+    dp, _, bc = merges("qft22_h22-12")
+    assert res.stats.sweeps == len(dp.buf.descs) - len(bc)
+    got = res.state.blocks.cpu().numpy()
+    ref, _ = orc.run_plan(plan, backend="c", nthreads=os.cpu_count() or 1)
+    assert np.max(np.abs(got - ref)) < 1e-12
