@@ -341,9 +341,21 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
         direct = {0, 1, 2, 3} <= {tout[k] for k in comp_l[:5]}
     if direct:
         w(f"  const u64 dst_t = {_deposit('t', [tout[k] for k in comp_l])};")
-    w("  double nrm = 0.0;")
+    # norm partial sums: NORM_ACC independent accumulators per sum, so the
+    # per-value terms need not form one serial FP64 chain through the tile
+    # (ncu, heaviest QV-30 sweep: the single chain's DFMAs hold 9.8% of the
+    # not-issued stall samples, but 4 chains measured no faster)
+    nacc = max(1, NORM_ACC)
+    w("  double " + ", ".join(["nrm = 0.0"] + [f"nrm_a{i} = 0.0" for i in range(1, nacc)]) + ";")
     if bcast is not None and bcast[2] not in (None, 0):
-        w("  double nrm2 = 0.0;")
+        w("  double " + ", ".join(["nrm2 = 0.0"] + [f"nrm2_a{i} = 0.0" for i in range(1, nacc)]) + ";")
+    rot = {"nrm": 0, "nrm2": 0}
+
+    def acc_name(base):
+        """Next accumulator of the sum `base` (round robin)."""
+        i = rot[base] % nacc
+        rot[base] += 1
+        return base if i == 0 else f"{base}_a{i}"
     w(f"  long long tile_id = blockIdx.x;")
 
     def origin(var):
@@ -405,7 +417,8 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
         order the merged sweep would multiply them (bit-identical values)."""
         if bcast is None:
             if not zero:
-                w(f"{ind}nrm = fma({val}.x, {val}.x, fma({val}.y, {val}.y, nrm));")
+                a = acc_name("nrm")
+                w(f"{ind}{a} = fma({val}.x, {val}.x, fma({val}.y, {val}.y, {a}));")
             if pred is None:
                 w(f"{ind}st_stream(state + chk({addr}), {val});")
             else:
@@ -428,13 +441,20 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
                 w(f"        const double2 {names[key]} = {e};")
             copies.append((f, names[key], True))
         if not zero and (boff is None or boff != 0):  # this sweep's own leaf: every value
-            w(f"        nrm = fma(({val}).x, ({val}).x, fma(({val}).y, ({val}).y, nrm));")
+            a = acc_name("nrm")
+            w(f"        {a} = fma(({val}).x, ({val}).x, fma(({val}).y, ({val}).y, {a}));")
         if pred is not None:
             w(f"        if ({pred}) {{")
+        if boff is not None:  # the merged leaf: the values stored (equal copies summed once)
+            mult = {}
+            for f, cv, live in copies:
+                if live:
+                    mult[cv] = mult.get(cv, 0) + 1
+            for cv, m in mult.items():
+                a = acc_name("nrm" if boff == 0 else "nrm2")
+                sq = f"fma({cv}.x, {cv}.x, {cv}.y * {cv}.y)"
+                w(f"        {a} = fma({_lit_raw(float(m))}, {sq}, {a});" if m > 1 else f"        {a} += {sq};")
         for f, cv, live in copies:
-            if live and boff is not None:  # the merged leaf: the values stored
-                acc = "nrm" if boff == 0 else "nrm2"
-                w(f"        {acc} = fma({cv}.x, {cv}.x, fma({cv}.y, {cv}.y, {acc}));")
             # the positions' F bits are cleared first: a kept region (st_keep) may set them
             w(f"        st_stream(state + chk((({addr}) & {~bmask & ((1 << 64) - 1)}ull) | {f}ull), {cv});")
         if pred is not None:
@@ -725,6 +745,10 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
     full = "0xffffffffu" if NT >= 32 else f"{(1 << NT) - 1}u"
     two = bcast is not None and bcast[2] not in (None, 0)
     for acc, dst, mult in [("nrm", "norm_out", 1)] + ([("nrm2", f"norm_out + {bcast[2]}", 1)] if two else []):
+        if nacc == 4:
+            w(f"    {acc} = ({acc} + {acc}_a1) + ({acc}_a2 + {acc}_a3);")
+        elif nacc > 1:
+            w(f"    {acc} = " + " + ".join([acc] + [f"{acc}_a{i}" for i in range(1, nacc)]) + ";")
         for o in (16, 8, 4, 2, 1):
             if o < NT:
                 w(f"    {acc} += __shfl_xor_sync({full}, {acc}, {o});")
@@ -745,6 +769,9 @@ def kernel_source(name: str, desc: dict, ops: list, coef: list, zero_init: int =
 GROUP_OFFSET = os.environ.get("SVB200_JIT_GROUP_OFFSET", "1") not in ("0", "false", "no")
 GROUPS_ONLY = int(os.environ["SVB200_JIT_GROUPS_ONLY"]) if os.environ.get("SVB200_JIT_GROUPS_ONLY") else None
 SKIP_DEAD = os.environ.get("SVB200_JIT_SKIP_DEAD", "1") not in ("0", "false", "no")
+# norm accumulators per thread (kernel_source); 4 measured equal to 1 on QV-30 and QFT-30
+# (655-657 ms, 3.09 ms either way: the chain's stalls are hidden), so the default keeps one
+NORM_ACC = int(os.environ.get("SVB200_JIT_NORM_ACC", "1"))
 # the last stage stores straight from registers when that coalesces (kernel_source)
 DIRECT_STORE = os.environ.get("SVB200_JIT_DIRECT_STORE", "1") not in ("0", "false", "no")
 # sparse sweeps: known-zero registers drop out of the arithmetic (kernel_source)
