@@ -26,8 +26,9 @@ assert jit.CHECK and executor.GUARD_AMPS, "run with SVB200_JIT_CHECK=1 SVB200_GU
 fams = json.load(gzip.open(ROOT / "tests/golden/families.json.gz", "rt"))
 plans = [(n, planmod.from_json(json.dumps(fams[n]["plan"]))) for n in ("qv20_h18-12", "qv21_h20-12", "qaoa20_h18-12",
                                                                        "sup20_h19-12")]
-plans += [(n, planmod.load(str(ROOT / "plans" / f"{n}.json.gz"))) for n in ("qft20_h18-12", "qft24_h22-12",
-                                                                           "mirror_qv24_h22-12")]
+# qft22/qft28 from |0>: their last sweep is broadcast-merged into the one before
+plans += [(n, planmod.load(str(ROOT / "plans" / f"{n}.json.gz")))
+          for n in ("qft20_h18-12", "qft22_h22-12", "qft24_h22-12", "qft28_h28-12", "mirror_qv24_h22-12")]
 bad = 0
 for name, plan in plans:
     ref = None
