@@ -209,8 +209,33 @@ def _devmap(jt: np.ndarray, tin) -> np.ndarray:
     return out
 
 
+LAST_MERGES = 0  # broadcast merges applied by the last emulate_plan (all devices)
+
+
+def _broadcast(state: np.ndarray, bc, keep) -> None:
+    """The merged store of executor._broadcast_merges: every value sweep j
+    stored (region `keep` of the masked bits, F bits otherwise clear) is
+    written, times its combination's constants, at each combination of F."""
+    fmask, copies = bc[0], bc[1]
+    km, kv = keep if keep is not None else (0, 0)
+    idx = np.arange(state.size, dtype=np.int64)
+    sel = idx[((idx & (fmask & ~km)) == 0) & ((idx & km) == kv)]
+    v = state[sel].copy()
+    base = sel & ~fmask
+    bits = [b for b in range(fmask.bit_length()) if (fmask >> b) & 1]
+    for j in range(1 << len(bits)):
+        f = sum(1 << bits[i] for i in range(len(bits)) if (j >> i) & 1)
+        val = np.zeros_like(v)
+        if f in copies:
+            val = v.copy()
+            for c in copies[f]:
+                val = val * c
+        state[base | f] = val
+
+
 def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog.RB, stable: bool = False,
-                 sparse: bool = False, kmax: int = prog.KMAX, localize: bool = False, fold: bool = True):
+                 sparse: bool = False, kmax: int = prog.KMAX, localize: bool = False, fold: bool = True,
+                 merge: bool = False):
     """Run a plan through the compiled device programs of `world` devices.
 
     Each device gets its own program (plan_device with its rank range);
@@ -241,6 +266,7 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
                 [(s.kind, s.task_id, s.swaps) for s in progs[0][1].steps]
     states = [np.zeros(1 << D, dtype=np.complex128) for _ in range(world)]
     states[0][0] = 1.0
+    bc_of = []  # per device: broadcast merges (executor._broadcast_merges)
     sp_of, lx_of, keep_of = [], [], []  # per device: descriptor -> (support, full_out) / load XOR / store mask
     for w, (geo, dp, descs, p) in enumerate(progs):
         sp = prog.sparse_start(dp, D, w == 0 or replicate) if sparse else {}
@@ -255,6 +281,14 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
         if sp:  # unwritten memory: any read outside the support would poison the result
             states[w][:] = np.nan
         sp_of.append(sp)
+        if merge and sp:
+            from paper_2509_14098_b200.executor import _broadcast_merges
+
+            bc_of.append(_broadcast_merges(dp, geo, sp, lx_of[-1], keep_of[-1], {}))
+        else:
+            bc_of.append({})
+    global LAST_MERGES
+    LAST_MERGES = sum(len(b) for b in bc_of)
     norms = np.zeros(max(progs[0][1].n_fused, 1))
     steps = {s.task_id: s for s in progs[0][1].steps}
     for task in plan.tasks:
@@ -263,10 +297,19 @@ def emulate_plan(plan, world: int = 1, check_layout: bool = True, rb: int = prog
             slot = sum(1 for t in plan.tasks[: plan.tasks.index(task)] if t.kind == "ApplyFused")
             for w, (geo, dp, descs, p) in enumerate(progs):
                 sw = {s.task_id: s for s in dp.steps}[task.id]
-                run_sweeps(states[w], descs[sw.first: sw.first + sw.count], p, norms,
-                           [sp_of[w].get(i) for i in range(sw.first, sw.first + sw.count)],
-                           [lx_of[w].get(i) for i in range(sw.first, sw.first + sw.count)],
-                           [keep_of[w].get(i) for i in range(sw.first, sw.first + sw.count)])
+                if not bc_of[w]:
+                    run_sweeps(states[w], descs[sw.first: sw.first + sw.count], p, norms,
+                               [sp_of[w].get(i) for i in range(sw.first, sw.first + sw.count)],
+                               [lx_of[w].get(i) for i in range(sw.first, sw.first + sw.count)],
+                               [keep_of[w].get(i) for i in range(sw.first, sw.first + sw.count)])
+                    continue
+                for i in range(sw.first, sw.first + sw.count):
+                    if i - 1 in bc_of[w]:
+                        continue  # merged into the sweep before it
+                    run_sweeps(states[w], descs[i:i + 1], p, None, [sp_of[w].get(i)], [lx_of[w].get(i)],
+                               [keep_of[w].get(i)])
+                    if i in bc_of[w]:
+                        _broadcast(states[w], bc_of[w][i], keep_of[w].get(i))
             if st.count == 0 and slot not in progs[0][1].norm_alias:
                 norms[slot] = norms[slot - 1] if slot else 1.0  # |0...0> (maybe not materialised yet)
         elif task.kind == "Exchange" and st.kind == "localize":

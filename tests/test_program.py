@@ -135,3 +135,24 @@ def test_localized_first_remap_matches_reference(grid_docs, grid_states, world, 
         used += prog.localize_applies(prog.plan_device(plan, geo, kmax=kmax), geo.D, world, geo.h)
         n += 1
     assert n > 20 and used > 5, (n, used)
+
+
+@pytest.mark.parametrize("world,kmax", [(1, 12), (1, 6), (2, 12), (4, 12), (2, 6), (4, 7)])
+def test_broadcast_merge_matches_reference(grid_docs, grid_states, world, kmax):
+    """Runs from |0...0> with the broadcast merge (executor._broadcast_merges):
+    a sweep that only expands dead bits is skipped and the sweep before it
+    stores every value at all combinations of those bits (also across a
+    folded localized remap), against the reference's blocks."""
+    n = merged = 0
+    for doc in _cases(grid_docs, grid_states, min_ranks=world):
+        plan = plan_from_doc(doc["plan"])
+        blocks, _ = program_emu.emulate_plan(plan, world=world, sparse=True, kmax=kmax, localize=world > 1,
+                                             merge=True)
+        err = float(np.max(np.abs(blocks - grid_states[doc["name"]])))
+        assert err < TOL, (doc["name"], world, err)
+        merged += program_emu.LAST_MERGES > 0
+        n += 1
+    assert n > 20, n
+    if kmax < 12:  # the grid plans (d <= 12) fit one 12-bit tile otherwise
+        assert merged > 0, (world, kmax)
+    print(f"world {world} kmax {kmax}: {n} plans, {merged} with a merge")
