@@ -103,11 +103,24 @@ def _cmul_lit(expr: str, c: complex) -> str:
     return f"cmulc({expr}, {_lit(cr)}, {_lit(ci)})"
 
 
+# 4-term sums as two independent 2-term chains plus one add (shorter FP64
+# dependency chains for one more DADD per component).  Measured on B200:
+# QV-30 656 -> 703 ms, so it is off (SVB200_JIT_SPLIT_LINCOMB=1)
+SPLIT_LINCOMB = os.environ.get("SVB200_JIT_SPLIT_LINCOMB", "0") not in ("0", "false", "no")
+
+
 def _lincomb(terms) -> str:
     """sum_k c_k * x_k for literal complex c_k (drops zero terms)."""
     terms = [(c, x) for c, x in terms if c != 0]
     if not terms:
         return "make_double2(0.0, 0.0)"
+    if SPLIT_LINCOMB and len(terms) >= 4:
+        h = len(terms) // 2
+        return f"cadd({_lincomb_chain(terms[:h])}, {_lincomb_chain(terms[h:])})"
+    return _lincomb_chain(terms)
+
+
+def _lincomb_chain(terms) -> str:
     c0, x0 = terms[0]
     acc = _cmul_lit(x0, c0)
     for c, x in terms[1:]:
