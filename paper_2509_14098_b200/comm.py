@@ -320,6 +320,30 @@ def release_arenas(group=None) -> int:
     return freed
 
 
+# the IPC-handle exchange of symmetric_buffer runs on a host (gloo) group:
+# an NCCL all-gather is ordered after the previous circuit's kernels on the
+# stream, and reading it back blocked the host until that circuit finished,
+# so a second circuit could not be enqueued while the first ran
+HOST_HANDSHAKE = os.environ.get("SVB200_HOST_HANDSHAKE", "1") not in ("0", "false", "no")
+_CTRL: dict = {}
+
+
+def _ctrl_group(group):
+    """A gloo group over the whole world for host-side metadata (None: use
+    `group` itself).  Only for the default group: new_group is collective
+    over every process, which all of them reach here only in that case."""
+    import torch.distributed as dist
+
+    if not HOST_HANDSHAKE or group is not None:
+        return None
+    if dist.get_backend() == "gloo":
+        return dist.group.WORLD
+    g = _CTRL.get("world")
+    if g is None:
+        g = _CTRL["world"] = dist.new_group(backend="gloo")
+    return g
+
+
 def symmetric_buffer(n: int, device, group):
     """A complex128 buffer of n amplitudes on `device` in storage every
     process of `group` has mapped; returns (tensor, PeerContext).
@@ -351,9 +375,12 @@ def symmetric_buffer(n: int, device, group):
     if world > FLAG_RANKS:
         raise ValueError(f"peer-memory remap supports at most {FLAG_RANKS} processes (got {world})")
     rec = np.frombuffer(arena.handle + int(arena.epoch).to_bytes(8, "little"), dtype=np.uint8)
-    mine = torch.from_numpy(rec.copy()).to(device)
+    ctrl = _ctrl_group(group)
+    mine = torch.from_numpy(rec.copy())
+    if ctrl is None:
+        mine = mine.to(device)
     allr = [torch.empty_like(mine) for _ in range(world)]
-    dist.all_gather(allr, mine, group=group)
+    dist.all_gather(allr, mine, group=ctrl if ctrl is not None else group)
     peers, peer_flags, epoch = {}, {}, 0
     for r, t in enumerate(allr):
         raw_all = bytes(t.cpu().numpy().tobytes())
