@@ -26,6 +26,10 @@ SVB_F double2 cmulr(double2 a, double cr) { return make_double2(a.x * cr, a.y * 
 SVB_F double2 cfmac(double2 a, double cr, double ci, double2 acc) {
   return make_double2(fma(a.x, cr, fma(-a.y, ci, acc.x)), fma(a.x, ci, fma(a.y, cr, acc.y)));
 }
+// acc + a * cr and acc + a * (i ci): real or imaginary literals (rx, ry, sqrt-X
+// blocks) need two FMAs, not four
+SVB_F double2 cfmar(double2 a, double cr, double2 acc) { return make_double2(fma(a.x, cr, acc.x), fma(a.y, cr, acc.y)); }
+SVB_F double2 cfmai(double2 a, double ci, double2 acc) { return make_double2(fma(-a.y, ci, acc.x), fma(a.x, ci, acc.y)); }
 SVB_F double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 SVB_F double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 

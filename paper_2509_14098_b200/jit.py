@@ -109,6 +109,10 @@ def _cmul_lit(expr: str, c: complex) -> str:
 SPLIT_LINCOMB = os.environ.get("SVB200_JIT_SPLIT_LINCOMB", "0") not in ("0", "false", "no")
 
 
+# real or imaginary coefficients accumulate with two FMAs (cfmar/cfmai)
+REAL_IMAG_FMA = os.environ.get("SVB200_JIT_REAL_IMAG_FMA", "1") not in ("0", "false", "no")
+
+
 def _lincomb(terms) -> str:
     """sum_k c_k * x_k for literal complex c_k (drops zero terms)."""
     terms = [(c, x) for c, x in terms if c != 0]
@@ -129,6 +133,10 @@ def _lincomb_chain(terms) -> str:
             acc = f"cadd({acc}, {x})"
         elif ci == 0.0 and cr == -1.0:
             acc = f"csub({acc}, {x})"
+        elif ci == 0.0 and REAL_IMAG_FMA:  # the dropped term is an exact zero
+            acc = f"cfmar({x}, {_lit(cr)}, {acc})"
+        elif cr == 0.0 and REAL_IMAG_FMA:
+            acc = f"cfmai({x}, {_lit(ci)}, {acc})"
         else:
             acc = f"cfmac({x}, {_lit(cr)}, {_lit(ci)}, {acc})"
     return acc
