@@ -1225,6 +1225,11 @@ def _emit_op(w, op, coef, stage, K, rb, half=None, zm: int = 0) -> int:
         b = int(op["b"])
         B = 1 << b
         M = np.asarray(coef[cf:cf + 16]).reshape(4, 4)
+        D = _column_phases(M) if FACTOR_U2 else None
+        if D is not None:  # M = R diag(D), R real/imaginary: 4 + 8 instead of 16 FP64 per amplitude
+            M = M / D[None, :]
+            M = np.where(np.abs(M.imag) <= 1e-15 * np.abs(M), M.real + 0j,
+                         np.where(np.abs(M.real) <= 1e-15 * np.abs(M), 1j * M.imag, M))
         for v in range(NR):
             if (v & A) or (v & B) or skip(v):
                 continue
@@ -1233,7 +1238,11 @@ def _emit_op(w, op, coef, stage, K, rb, half=None, zm: int = 0) -> int:
             if not live:
                 continue
             w("      {")
-            w("        const double2 " + ", ".join(f"a{c} = x[{idx[c]}]" for c in live) + ";")
+            if D is None:
+                w("        const double2 " + ", ".join(f"a{c} = x[{idx[c]}]" for c in live) + ";")
+            else:
+                w("        const double2 " + ", ".join(f"a{c} = {_cmul_lit(f'x[{idx[c]}]', D[c])}" for c in live)
+                  + ";")
             for r in range(4):
                 w(f"        x[{idx[r]}] = {_lincomb([(M[r, c], f'a{c}') for c in live])};")
             w("      }")
@@ -1251,6 +1260,35 @@ def _emit_op(w, op, coef, stage, K, rb, half=None, zm: int = 0) -> int:
         w("    }")
     w("    }")
     return woke & zm
+
+
+# a 4x4 whose columns are each a phase times a real/imaginary vector (QAOA:
+# rx (x) rx after a ZZ phase) runs as a diagonal then a real/imaginary 4x4
+FACTOR_U2 = os.environ.get("SVB200_JIT_FACTOR_U2", "1") not in ("0", "false", "no")
+
+
+def _column_phases(M: np.ndarray):
+    """D with M = R diag(D), every entry of R real or imaginary, when M
+    itself is not (else None)."""
+    def ri(z):
+        return z.real == 0 or z.imag == 0
+
+    if all(ri(z) for z in M.ravel()):
+        return None
+    D = np.ones(4, dtype=np.complex128)
+    for c in range(4):
+        col = M[:, c]
+        nz = [z for z in col if z != 0]
+        if not nz:
+            continue
+        ph = nz[0] / abs(nz[0])
+        q = col / ph
+        # entries within rounding of the real or imaginary axis count; the
+        # factored product equals M to ~1 ulp (checked by the parity tests)
+        if not all(abs(z.imag) <= 1e-15 * abs(z) or abs(z.real) <= 1e-15 * abs(z) for z in q):
+            return None
+        D[c] = ph
+    return D
 
 
 def _emit_dfs(w, a: int, nt: int, c: list, fused_h: bool, rb: int, half=None, zm: int = 0) -> None:
