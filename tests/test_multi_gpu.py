@@ -39,13 +39,16 @@ def test_dist_parity(world, remap):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_dist_parity_colocated(world):
     """The inter-process remap on a one-GPU box: `world` processes share
     cuda:0 (gloo control plane), map each other's state with CUDA IPC and
     swap through the same bulk-copy kernel, flag epochs and overlapped
     chunks as across GPUs; checked against the goldens, the oracle, the
-    closed-form QFT and mirrors, plus sharded compare/fidelity/sampling."""
+    closed-form QFT and mirrors, plus sharded compare/fidelity/sampling.
+    world 8: QFT-33 over eight processes (128 GiB on the one GPU), an m = 3
+    remap from |x> and the localized remap with an eight-way broadcast
+    merge from |0...0> -- the 8-GPU code paths without an 8-GPU box."""
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
     env = dict(os.environ, SVB200_REMAP="peer")
