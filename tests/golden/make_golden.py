@@ -263,6 +263,10 @@ BENCH = [
     ("mirror_qv31_h29-12", lambda: workloads.mirror(workloads.quantum_volume(31, seed=10, depth=12)), [29, 12]),
     ("mirror_sup31_h29-12", lambda: workloads.mirror(workloads.random_supremacy(31, seed=11)), [29, 12]),
     ("mirror_qaoa31_h29-12", lambda: workloads.mirror(workloads.qaoa_maxcut(31, seed=12, p=2)), [29, 12]),
+    # 8 ranks of 2^28 (world-8 remaps with m up to 3; eight processes can share one GPU)
+    ("mirror_qv31_h28-12", lambda: workloads.mirror(workloads.quantum_volume(31, seed=14, depth=10)), [28, 12]),
+    ("mirror_sup31_h28-12", lambda: workloads.mirror(workloads.random_supremacy(31, seed=15)), [28, 12]),
+    ("mirror_qaoa31_h28-12", lambda: workloads.mirror(workloads.qaoa_maxcut(31, seed=16, p=2)), [28, 12]),
     # the exact QV-30 bench circuit inverted: forward + inverse from a random basis state on one GPU
     ("qv30inv_h30-12", lambda: workloads.inverse(workloads.quantum_volume(30, seed=34)), [30, 12]),
     # 34-qubit QV mirror on 2 GPUs (cfg3 shape, half depth each way): tools/dist_check.py --qv34

@@ -98,7 +98,9 @@ def scale_checks(me, world):
         del res
     # mirror circuits U U^dagger over several GPUs (QV with 4-5 remaps, supremacy): every
     # amplitude must return to |0...0>, checked shard by shard
-    mirrors = ["mirror_qv30_h29-12", "mirror_qv31_h29-12", "mirror_sup31_h29-12", "mirror_qaoa31_h29-12"]
+    mirrors = ["mirror_qv30_h29-12", "mirror_qv31_h29-12", "mirror_sup31_h29-12", "mirror_qaoa31_h29-12",
+               # 8 ranks: m = 3 remaps (every partner of a rank at world 8)
+               "mirror_qv31_h28-12", "mirror_sup31_h28-12", "mirror_qaoa31_h28-12"]
     if "--qv34" in sys.argv:  # 34 qubits: 2 GPUs of 128 GiB each
         mirrors.append("mirror_qv34_h33-12")
     for name in mirrors:
