@@ -97,7 +97,7 @@ def scale_checks(me, world):
             print(name, "x", hex(x), "closed-form err", err, "remaps", len(res.stats.exchanges), flush=True)
         del res
     # mirror circuits U U^dagger over several GPUs (QV with 4-5 remaps, supremacy): every
-    # amplitude must return to |0...0>, checked shard by shard
+    # amplitude must return to the start |x>, checked shard by shard
     mirrors = ["mirror_qv30_h29-12", "mirror_qv31_h29-12", "mirror_sup31_h29-12", "mirror_qaoa31_h29-12",
                # 8 ranks: m = 3 remaps (every partner of a rank at world 8)
                "mirror_qv31_h28-12", "mirror_sup31_h28-12", "mirror_qaoa31_h28-12"]
@@ -113,21 +113,32 @@ def scale_checks(me, world):
 
         comm.release_arenas()
         torch.cuda.empty_cache()
-        res = run_plan(plan)
+        # U U^dagger |x> = |x> from a random basis state: every amplitude and
+        # its storage position are checked (|0...0> would hide a wrong relabel
+        # or final materialisation: it is invariant under bit permutations)
+        x = (0x9E3779B97F4A7C15 * (len(name) + 7)) & ((1 << plan.d) - 1)
+        rows = (1 << plan.g) // world
+        init = basis_blocks(plan, x, me * rows, rows, "cpu" if "--colocate" in sys.argv else "cuda")
+        res = run_plan(plan, initial=init)
+        del init
+        L = plan.d - plan.g
+        fin = res.state.layouts[res.state.phase]
+        f = 0
+        for q in range(plan.d):
+            if (x >> (plan.d - 1 - q)) & 1:
+                f |= 1 << (plan.d - 1 - fin[q])
         flat = res.state.blocks.reshape(-1)
+        local = f - (res.state.rank_base << L)
+        if 0 <= local < flat.numel():
+            flat[local] -= 1.0  # the one amplitude that must be 1
         err = torch.zeros(1, dtype=torch.float64, device=flat.device)
         for off in range(0, flat.numel(), 1 << 26):  # chunked: no full-size temporaries
-            part = flat[off:off + (1 << 26)]
-            if off == 0 and res.state.rank_base == 0:
-                err = torch.maximum(err, (part[0] - 1).abs().reshape(1))
-                part = part[1:]
-            if part.numel():
-                err = torch.maximum(err, part.abs().max().reshape(1))
+            err = torch.maximum(err, flat[off:off + (1 << 26)].abs().max().reshape(1))
         dist.all_reduce(err, op=dist.ReduceOp.MAX)
         n += 1
         bad += float(err.item()) > 1e-10
         if me == 0:
-            print(name, "mirror |0...0> err", float(err.item()), "remaps", len(res.stats.exchanges),
+            print(name, f"mirror |x> (x={x:#x}) err", float(err.item()), "remaps", len(res.stats.exchanges),
                   "ms", round(1e3 * (res.stats.compute_seconds + res.stats.exchange_seconds), 1), flush=True)
         del res, flat
     # sharded compare / fidelity vs the gathered reference compare
