@@ -228,7 +228,7 @@ class ClockSampler:
 # CPU reference arm
 # ---------------------------------------------------------------------------
 
-CPU_SAMPLE_PLAN = "qft22_h22-12"  # same family and [d, 12] hierarchy, bounded CPU time
+CPU_SAMPLE_PLAN = os.environ.get("SVB200_REF_SAMPLE", "qft22_h22-12")  # same family and [d, 12] hierarchy, bounded CPU time
 
 
 def cpu_reference_step(plan, backend: str) -> float:
