@@ -51,6 +51,20 @@ def test_dist_parity_colocated(world):
     merge from |0...0> -- the 8-GPU code paths without an 8-GPU box."""
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
+    # the processes share this GPU with the pytest process: return what
+    # earlier tests left cached (compiled plans, pooled state buffers)
+    import gc
+
+    from paper_2509_14098_b200 import comm, executor
+
+    executor._compile_cache.clear()
+    gc.collect()
+    comm.release_arenas()
+    torch.cuda.empty_cache()
+    if world == 8:  # QFT-33 over eight processes: 8 x 16 GiB on this one GPU
+        free, _ = torch.cuda.mem_get_info()
+        if free < (8 * 16 + 24) << 30:
+            pytest.skip(f"needs ~152 GiB free on the GPU ({free >> 30} GiB)")
     env = dict(os.environ, SVB200_REMAP="peer")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "tools" / "dist_check.py"),
