@@ -263,10 +263,25 @@ def cpu_baseline_line(min_seconds: float = 10.0, sample: str = CPU_SAMPLE_PLAN) 
             "seconds": t}
 
 
-def _ref_worker(backend: str, n_warm: int, n_steps: int, barrier, out) -> None:
+# the reference arm keeps a run within a few minutes: with many steps each
+# step samples a smaller circuit of the same family and hierarchy
+REF_BUDGET_S = float(os.environ.get("SVB200_REF_BUDGET_S", "240"))
+REF_STEP_S = {"qft22_h22-12": 5.3, "qft20_h18-12": 1.8}  # one circuit per core, 16-core GPU boxes
+
+
+def ref_sample(steps: int, warmup: int) -> str:
+    if "SVB200_REF_SAMPLE" in os.environ:
+        return CPU_SAMPLE_PLAN
+    for name in ("qft22_h22-12", "qft20_h18-12"):
+        if (steps + warmup) * REF_STEP_S[name] <= REF_BUDGET_S:
+            return name
+    return "qft20_h18-12"
+
+
+def _ref_worker(sample: str, backend: str, n_warm: int, n_steps: int, barrier, out) -> None:
     """One host core: warm-up circuits, then (after every worker is warm)
     n_steps timed circuits of the sample plan; reports their wall time."""
-    plan = load_plan(CPU_SAMPLE_PLAN)
+    plan = load_plan(sample)
     for _ in range(n_warm):
         cpu_reference_step(plan, backend)
     barrier.wait()
@@ -287,13 +302,14 @@ def run_reference_arm(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return  # only rank 0 runs the CPU baseline under torchrun
-    plan = load_plan(CPU_SAMPLE_PLAN)
+    sample = ref_sample(args.steps, args.warmup)
+    plan = load_plan(sample)
     backend, kind = cpu_backend()
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     cores = int(os.environ.get("SVB200_REF_CORES", cores))
     ctx = mp.get_context("fork")  # this process never touched CUDA
     barrier, out = ctx.Barrier(cores), ctx.Queue()
-    procs = [ctx.Process(target=_ref_worker, args=(backend, args.warmup, args.steps, barrier, out))
+    procs = [ctx.Process(target=_ref_worker, args=(sample, backend, args.warmup, args.steps, barrier, out))
              for _ in range(cores)]
     for p in procs:
         p.start()
@@ -308,14 +324,15 @@ def run_reference_arm(args) -> None:
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": workload_name(args.workload, max(args.gpus, 1))[0],
-                   "sample": f"{CPU_SAMPLE_PLAN}: the same QFT family and [d, 12] hierarchy at "
-                             f"{plan.d} qubits (the full workload takes ~70 min per run on one core); "
+                   "sample": f"{sample}: the same QFT family and [d, 12] hierarchy at "
+                             f"{plan.d} qubits (the full workload takes ~70 min per run on one core; "
+                             f"QFT-20 instead of QFT-22 when {args.steps} steps would exceed ~{REF_BUDGET_S:.0f} s); "
                              "value = algorithmic bytes / time, size-normalised like the GPU arm",
                    "note": "reference run_plan semantics with the reference's compiled _core.pyx "
                            f"kernels, which are single-threaded: {cores} independent copies, one per "
                            "host core, each step one circuit on every core"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"{CPU_SAMPLE_PLAN} full plan per core per step ({cores} processes), "
+                         "sample": f"{sample} full plan per core per step ({cores} processes), "
                                    f"per-core circuit {1e3 * total / args.steps:.0f} ms"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
