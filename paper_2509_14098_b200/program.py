@@ -114,6 +114,7 @@ class Dense1:
     ctrl: dict  # device bit -> required value (0/1)
     noop: bool = False  # a constant-0 control made it identity on this device
     perm: bool = False  # structurally a bit flip (x, cx, ccx): costs no FP64
+    gctl: bool = False  # had rank-global controls (resolved differently per device)
 
 
 @dataclass
@@ -257,11 +258,12 @@ def resolve_entry(entry: dict, layout, geo: DeviceGeometry) -> list:
     if block is not None and len(tgt) == 1:
         perm = bool(np.array_equal(block, _X))
         return [Dense1(free_bits[tgt[0]], np.eye(2, dtype=np.complex128) if noop else block,
-                       {} if noop else {free_bits[j]: 1 for j in ctl}, noop=noop, perm=perm)]
+                       {} if noop else {free_bits[j]: 1 for j in ctl}, noop=noop, perm=perm,
+                       gctl=bool(fixed))]
     if k == 1:
         perm = bool(np.array_equal(sub, _X))
         return [Dense1(free_bits[0], np.eye(2, dtype=np.complex128) if noop else sub, {},
-                       noop=noop, perm=perm)]
+                       noop=noop, perm=perm, gctl=bool(fixed))]
     raise NotImplementedError(f"no device decomposition for {gate.kind} on {k} free slots")
 
 
@@ -345,6 +347,10 @@ def _bits_of(pr) -> set:
     return set()
 
 
+# pair blocks of bit flips and phases whose flips cancel become phases (fuse_prims)
+DIAG_PAIRS = os.environ.get("SVB200_DIAG_PAIRS", "1") not in ("0", "false", "no")
+
+
 def fuse_prims(prims: list, owners: list | None = None):
     """Merge runs of gates confined to one qubit pair into a single 4x4 (e.g.
     the u,u,cx,u,u,cx,u,u,cx,u,u form of an SU(4)).
@@ -379,6 +385,21 @@ def fuse_prims(prims: list, owners: list | None = None):
         dense = [p for p in ps if isinstance(p, Dense1)]
         nonperm = [p for p in dense if not p.perm]
         bits = sorted(blk["bits"])
+        if DIAG_PAIRS and len(bits) == 2 and dense and not nonperm and not any(p.gctl for p in dense):
+            # bit flips and phases only (QAOA's cx rz cx): when the flips
+            # cancel, the block is a diagonal -- phases, no data movement
+            # (a runtime-controlled flip is a conditional register swap)
+            a, b = bits[1], bits[0]
+            m = np.eye(4, dtype=np.complex128)
+            for p in ps:
+                m = _embed2(p, a, b) @ m
+            if not np.any(m - np.diag(np.diag(m))):
+                d = np.diag(m)
+                for fb, c in (((), d[0]), ((b,), d[1] / d[0]), ((a,), d[2] / d[0]),
+                              ((a, b), d[3] * d[0] / (d[1] * d[2]))):
+                    if c != 1:
+                        emit(Factor(fb, complex(c)), top)
+                return
         if len(nonperm) >= 2 and len(bits) == 2:
             a, b = bits[1], bits[0]
             m = np.eye(4, dtype=np.complex128)
