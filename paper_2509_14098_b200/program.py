@@ -347,6 +347,8 @@ def _bits_of(pr) -> set:
     return set()
 
 
+# the last sweep before a remap reserves tile room to park the remap's qubits on top
+PARK_FIRST = os.environ.get("SVB200_PARK_FIRST", "1") not in ("0", "false", "no")
 # pair blocks of bit flips and phases whose flips cancel become phases (fuse_prims)
 DIAG_PAIRS = os.environ.get("SVB200_DIAG_PAIRS", "1") not in ("0", "false", "no")
 
@@ -943,16 +945,27 @@ def plan_device(plan, geo: DeviceGeometry, kmax: int = KMAX, low: int = LOW_RUN_
             # store can park them on the low bits
             look = _Lookahead(stream, base + j, NL)
             tile = set(need)
+
+            def park_exchange():  # let the store park the next remap's qubits on top
+                for r in look.exchange:
+                    if len(tile) + 2 <= K:
+                        tile.add(trial[r])
+                for p_top in range(NL - 1, NL - 1 - len(look.exchange), -1):
+                    if len(tile) < K:
+                        tile.add(p_top)
+
+            # the sweep that ends the segment reserves room for that first: no
+            # gate may need the remap's qubits (phase-only blocks), and the
+            # next-needed padding would otherwise fill the tile
+            before_remap = j >= n and bool(look.exchange) and PARK_FIRST
+            if before_remap:
+                park_exchange()
             for r in sorted(look.first_use, key=look.first_use.get):
                 if len(tile) >= K:
                     break
                 tile.add(trial[r])
-            for r in look.exchange:  # let the store park the next remap's qubits on top
-                if len(tile) + 2 <= K:
-                    tile |= {trial[r]}
-            for p_top in range(NL - 1, NL - 1 - len(look.exchange), -1):
-                if len(tile) < K:
-                    tile.add(p_top)
+            if not before_remap:
+                park_exchange()
             _pad_displaced(tile, trial, look, K, NL)
             for b in range(D):
                 if len(tile) >= K:
